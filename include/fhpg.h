@@ -1,0 +1,143 @@
+/*
+ * fhpg.h — C ABI of the B200 FHP lattice-gas engine (libfhpg.so).
+ *
+ * This is the drop-in boundary for the reference's evolution path:
+ *
+ *   std::uint64_t fhp::advance(Lattice& lat, const CollisionTable& table,
+ *                              const SimConfig& cfg, int first_step,
+ *                              int step_count);
+ *     (/root/reference/proj/core/include/fhp/step.hpp:46-47,
+ *      proj/core/src/step.cpp:103-133)
+ *
+ * A `case Backend::Cuda:` in that switch uploads
+ * lat.src() and the obstacle mask, sets the table, calls fhpg_advance and
+ * downloads the result into lat.src(). The framework's own C++ host layer
+ * (paper_1208_2428_b200/host, namespace fhp_b200) keeps the state resident on
+ * the device between calls instead.
+ *
+ * Plain C types only. Every function returns 0 on success, FHPG_EINVAL (2)
+ * for the conditions the reference reports with std::invalid_argument and
+ * FHPG_ERUNTIME (3) for the ones it reports with std::runtime_error (CUDA
+ * failures included) — the same split the reference CLI maps to exit codes 2
+ * and 3 (proj/tools/fhp_main.cpp:171-182). fhpg_last_error() gives the
+ * message of the last failure on the calling thread.
+ *
+ * Byte layout of every host buffer: row-major rows of W node bytes (the
+ * reference's storage columns 1..W), consecutive rows `stride` bytes apart;
+ * pass lat.src() + 1 with stride W + 2 for a reference Lattice. Node byte:
+ * bits 0-5 movers NW,NE,E,SE,SW,W, bit 6 rest, bit 7 obstacle
+ * (node_state.hpp:9-20). Obstacle masks: one byte per node, nonzero = solid
+ * (the Lattice's obstacle_ vector, lattice.hpp:67).
+ */
+#ifndef FHPG_H
+#define FHPG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FHPG_OK 0
+#define FHPG_EINVAL 2
+#define FHPG_ERUNTIME 3
+
+typedef struct fhpg_engine fhpg_engine;
+
+/* Engine for a whole W x H lattice on the current CUDA device.
+ * Replaces Lattice::Lattice (lattice.cpp:10-17): W >= 1, H >= 3. */
+int fhpg_create(int width, int height, fhpg_engine** out);
+
+/* Engine for the row strip [row_begin, row_end) of a W x H lattice on CUDA
+ * device `device` (multi-GPU row strips, the device analog of the strips
+ * backend's worker rows, backends.cpp:140-145). Halo rows row_begin-1 and
+ * row_end are filled by the caller through fhpg_halo() before every step. */
+int fhpg_create_strip(int width, int height, int row_begin, int row_end, int device,
+                      fhpg_engine** out);
+
+void fhpg_destroy(fhpg_engine* e);
+
+/* Thread-local message of the last failure ("" if none). */
+const char* fhpg_last_error(void);
+
+/* Stream all engine work is enqueued on (a cudaStream_t); NULL = the
+ * engine's own stream. */
+int fhpg_set_stream(fhpg_engine* e, void* cuda_stream);
+
+/* 512-entry collision table, index (chirality << 8) | state
+ * (CollisionTable, collision.hpp:17-23). Rejected (FHPG_EINVAL) if any entry
+ * changes bit 7: the engine keeps the obstacle flag in bit 7 of the state
+ * (the reference re-derives it from the mask during motion, step.cpp:50). */
+int fhpg_set_table(fhpg_engine* e, const uint8_t table[512]);
+
+/* Obstacle mask for the engine's rows (Lattice::set_obstacle, lattice.cpp:19-30). */
+int fhpg_set_obstacles(fhpg_engine* e, const uint8_t* mask, size_t stride);
+
+/* Copy the engine's rows from / to host memory (bit 7 included). An upload
+ * is kept byte-exact until the first step; stepping derives bit 7 from the
+ * obstacle mask exactly like the reference's motion pass. */
+int fhpg_upload(fhpg_engine* e, const uint8_t* state, size_t stride);
+int fhpg_download(fhpg_engine* e, uint8_t* state, size_t stride);
+
+/* init_lattice(cfg) on the device, bit-exact with lattice.cpp:44-93: walls on
+ * global rows 0 and H-1, the obstacle mask set by fhpg_set_obstacles (the
+ * geometry), counter-RNG fill of every other node. Also sets bit 7. */
+int fhpg_init(fhpg_engine* e, uint64_t seed, double fill_density);
+
+/* The hot path: step_count full steps with global step indices
+ * first_step .. first_step+step_count-1 (step.cpp:95-133). force_thr is the
+ * bernoulli threshold of rng.hpp:37-42 (fhpg_bernoulli_threshold(force_p)),
+ * 0 = no forcing. step_count <= 0 is a no-op. Blocks until done and returns
+ * the accepted forcing swaps in *swaps (may be NULL). */
+int fhpg_advance(fhpg_engine* e, uint64_t seed, uint64_t force_thr, int64_t first_step,
+                 int64_t step_count, uint64_t* swaps);
+
+/* Same, enqueue only: swaps accumulate on the device, read with fhpg_swaps. */
+int fhpg_advance_async(fhpg_engine* e, uint64_t seed, uint64_t force_thr, int64_t first_step,
+                       int64_t step_count);
+
+/* Synchronise and read (optionally reset) the device swap counter. */
+int fhpg_swaps(fhpg_engine* e, uint64_t* swaps, int reset);
+
+/* Block until all enqueued engine work is done. */
+int fhpg_synchronize(fhpg_engine* e);
+
+/* rng.hpp:37-42 threshold: p >= 1 ? 2^32 : (uint64_t)(p * 2^32). */
+uint64_t fhpg_bernoulli_threshold(double p);
+
+/* Integer observables of the engine's rows (observables.cpp:27-47):
+ * mass = sum popcount(s & 0x7F) over all nodes, momentum over fluid nodes. */
+int fhpg_reduce_global(fhpg_engine* e, int64_t* mass, int64_t* px, int64_t* py);
+
+/* coarse_grain integer sums (observables.cpp:49-82) on the GLOBAL cell grid
+ * cells_x = ceil(W/B), cells_y = ceil((H-2)/B), row-major; a strip adds only
+ * its own rows (sum the arrays over strips). */
+int fhpg_reduce_cells(fhpg_engine* e, int block, int32_t* nodes, int32_t* particles,
+                      int64_t* px, int64_t* py);
+
+/* velocity_profile integer sums (observables.cpp:84-102): for global interior
+ * row r (1..H-2) entry r-1 = (sum px over fluid nodes, fluid node count);
+ * only the engine's own rows are written. */
+int fhpg_reduce_rows(fhpg_engine* e, int64_t* px, int32_t* fluid_count);
+
+/* Device pointers of the current state's boundary rows and halo rows for
+ * the halo exchange of a strip (each row_bytes long, valid until the next
+ * step): send_top = first owned row, send_bottom = last owned row,
+ * recv_top = halo row above, recv_bottom = halo row below. */
+int fhpg_halo(fhpg_engine* e, void** send_top, void** send_bottom, void** recv_top,
+              void** recv_bottom, size_t* row_bytes);
+
+/* Introspection: W, H, row_begin, row_end, which step kernel runs
+ * (1 = fast streaming path, 0 = generic), and the number of step-kernel
+ * launches enqueued so far. */
+int fhpg_info(fhpg_engine* e, int* width, int* height, int* row_begin, int* row_end,
+              int* fast_path, uint64_t* step_launches);
+
+/* Testing aid: force the generic (one-thread-per-site) step kernel. */
+int fhpg_force_generic(fhpg_engine* e, int on);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FHPG_H */

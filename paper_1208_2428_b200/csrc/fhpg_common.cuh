@@ -1,0 +1,73 @@
+// fhpg_common.cuh — node encoding and the counter RNG, bit-exact with the
+// reference (proj/core/include/fhp/node_state.hpp, rng.hpp), usable from host
+// and device code.
+#pragma once
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define FHPG_HD __host__ __device__ __forceinline__
+#else
+#define FHPG_HD inline
+#endif
+
+namespace fhpg {
+
+// node_state.hpp:13-15
+constexpr uint32_t kMovingMask = 0x3F;
+constexpr uint32_t kRestBit = 0x40;
+constexpr uint32_t kObstacleBit = 0x80;
+
+// rng.hpp:11, :13
+enum Purpose : uint64_t { kInit = 0, kForcing = 1, kChirality = 2 };
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kC1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kC2 = 0x94D049BB133111EBull;
+
+// rng.hpp:15-23 — splitmix64 finaliser, split as mix64(z) = fin64(z + gamma)
+// so the "+ gamma" can be folded into per-column precomputed keys.
+FHPG_HD uint64_t fin64(uint64_t z) {
+  z ^= z >> 30;
+  z *= kC1;
+  z ^= z >> 27;
+  z *= kC2;
+  z ^= z >> 31;
+  return z;
+}
+FHPG_HD uint64_t mix64(uint64_t z) { return fin64(z + kGamma); }
+
+// rng.hpp:25-33
+FHPG_HD uint64_t node_random(uint64_t seed, uint64_t purpose, uint64_t step, uint64_t x,
+                             uint64_t y) {
+  uint64_t z = mix64(seed + kGamma * purpose);
+  z = mix64(z + step);
+  z = mix64(z + x);
+  return mix64(z + y);
+}
+
+// Per-(purpose, step) prefix of node_random: mix64(mix64(seed+g*p)+step).
+FHPG_HD uint64_t step_key(uint64_t seed, uint64_t purpose, uint64_t step) {
+  return mix64(mix64(seed + kGamma * purpose) + step);
+}
+
+// Per-column key: node_random(seed,p,step,x,y) == fin64(column_key + y).
+FHPG_HD uint64_t column_key(uint64_t step_key_value, uint64_t x) {
+  return mix64(step_key_value + x) + kGamma;
+}
+
+// Bit 0 of fin64(z), computing only what that bit depends on: bit 0 of the
+// result is bit0 ^ bit31 of z2 = z1' * C2, whose low 32 bits depend only on
+// the low 32 bits of z1' = z1 ^ (z1 >> 27).
+FHPG_HD uint32_t fin64_bit0(uint64_t z) {
+  z ^= z >> 30;
+  z *= kC1;
+  const uint32_t lo = static_cast<uint32_t>(z) ^ static_cast<uint32_t>(z >> 27);
+  const uint32_t p = lo * static_cast<uint32_t>(kC2);
+  return (p ^ (p >> 31)) & 1u;
+}
+
+// rng.hpp:37-42: bernoulli(word, p) == (word >> 32) < threshold(p).
+inline uint64_t bernoulli_threshold(double p) {
+  return p >= 1.0 ? (1ull << 32) : static_cast<uint64_t>(p * 4294967296.0);
+}
+
+}  // namespace fhpg

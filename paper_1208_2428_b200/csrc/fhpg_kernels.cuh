@@ -1,0 +1,68 @@
+// fhpg_kernels.cuh — device kernels of the FHP engine and their host launchers.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace fhpg {
+
+// Device lattice view of one strip of rows. The buffer holds nrows+2 rows of
+// `pitch` bytes: local row -1 (top halo), rows 0..nrows-1 (owned), row nrows
+// (bottom halo). Halo rows are zero where the strip touches the global grid
+// edge (the reference's "out-of-grid rows contribute nothing", step.cpp:47)
+// and hold the neighbour strip's boundary row otherwise. `base` points at
+// local row 0, column 0 (reference storage column 1).
+struct StepArgs {
+  const uint8_t* src;
+  uint8_t* dst;
+  size_t pitch;
+  int W;
+  int nrows;
+  long long row0;            // global index of local row 0 (row parity, RNG y)
+  const uint8_t* table;      // 512-entry collision table (device)
+  const uint64_t* zc;        // chirality column keys for this step, index x-1
+  const uint64_t* zf;        // forcing column keys for this step (thr > 0)
+  uint64_t thr;              // bernoulli threshold, 0 = no forcing
+  unsigned long long* swaps; // accumulated accepted forcing swaps
+  uint64_t* zc_next;         // column keys of the next step (may be null)
+  uint64_t* zf_next;
+  uint64_t kc_next, kf_next; // step keys of the next step
+  int seg_rows;              // rows per warp task (fast path)
+  int nbands;                // 512-column bands (fast path)
+  int row_lo, row_hi;        // local row range to update, [row_lo, row_hi)
+};
+
+// Kernel selection for a lattice width.
+bool fast_path_ok(int W);
+
+// One time step (motion -> collision -> forcing) over rows [row_lo,row_hi).
+// Returns the number of kernel launches enqueued.
+int launch_step(const StepArgs& a, int num_sms, cudaStream_t st, bool force_generic);
+
+// Column keys for one step: zc[i] = column_key(kc, i+1), same for zf.
+void launch_column_keys(uint64_t* zc, uint64_t* zf, uint64_t kc, uint64_t kf, int W,
+                        cudaStream_t st);
+
+// src bit 7 := obstacle mask (bytes 0/1), bits 0-6 untouched, on owned rows.
+void launch_apply_mask(uint8_t* base, const uint8_t* mask, size_t pitch, int W, int nrows,
+                       cudaStream_t st);
+
+// init_lattice on device (lattice.cpp:44-93) for owned rows of a strip.
+void launch_init(uint8_t* base, const uint8_t* mask, size_t pitch, int W, int nrows,
+                 long long row0, long long H, uint64_t seed, uint64_t thr, cudaStream_t st);
+
+// Reductions. acc: 3 x int64 (mass, px, py) over owned rows (observables.cpp:27-47).
+void launch_reduce_global(const uint8_t* base, size_t pitch, int W, int nrows,
+                          long long* acc, cudaStream_t st);
+// Per cell (nodes, particles, px, py) over global interior rows 1..H-2
+// (observables.cpp:49-82); output arrays are the full global cell grid.
+void launch_reduce_cells(const uint8_t* base, size_t pitch, int W, int nrows, long long row0,
+                         long long H, int B, int* nodes, int* particles, long long* px,
+                         long long* py, cudaStream_t st);
+// Per owned interior row (px sum, fluid count) (observables.cpp:84-102);
+// index = global row - 1.
+void launch_reduce_rows(const uint8_t* base, size_t pitch, int W, int nrows, long long row0,
+                        long long H, long long* px, int* fluid, cudaStream_t st);
+
+}  // namespace fhpg

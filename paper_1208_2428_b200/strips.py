@@ -1,0 +1,102 @@
+"""Row-strip decomposition across GPUs (one process per GPU).
+
+The reference's strips backend splits interior rows into balanced strips,
+worker 0 also owning wall row 0 and the last worker row H-1
+(make_strip_plan backends.cpp:20-36, worker_rows :140-145), and relies on a
+shared address space for the rows across strip borders (run_strips
+:149-219). Here each strip lives on its own GPU (fhpg_create_strip) and the
+one-row halos (pull motion reaches rows r-1 and r+1 only) are
+exchanged every step with point-to-point transfers over NVLink
+(torch.distributed / NCCL), ordered on the engine's stream. Every random
+decision is keyed by global (x, y, step), so any strip count gives the
+single-GPU bits exactly.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def strip_rows(height: int, n: int):
+    """make_strip_plan + worker_rows: [(row_begin, row_end)] for n strips."""
+    interior = height - 2
+    if n < 1:
+        raise ValueError("strip count must be >= 1")
+    if n > interior:
+        raise ValueError("strip count exceeds interior row count")
+    base, extra = divmod(interior, n)
+    rows, r = [], 1
+    for i in range(n):
+        k = base + (1 if i < extra else 0)
+        rows.append([r, r + k])
+        r += k
+    rows[0][0] = 0
+    rows[-1][1] = height
+    return [tuple(x) for x in rows]
+
+
+class _DeviceBytes:
+    """__cuda_array_interface__ view of `n` device bytes (no copy)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def device_row(ptr: int, n: int, device: int) -> torch.Tensor:
+    return torch.as_tensor(_DeviceBytes(ptr, n), device=f"cuda:{device}")
+
+
+def engine_halo_tensors(engine, device: int):
+    """(send_top, send_bottom, recv_top, recv_bottom) uint8 CUDA tensors."""
+    (st, sb, rt, rb), n = engine.halo()
+    return tuple(device_row(p, n, device) for p in (st, sb, rt, rb))
+
+
+def exchange_halos(send_top, send_bottom, recv_top, recv_bottom, rank: int, world: int,
+                   group=None):
+    """Send the first/last owned rows to the strips above/below and receive
+    their boundary rows into the halo rows (no-op at the global edges)."""
+    ops = []
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, send_top, rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, recv_top, rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.isend, send_bottom, rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, recv_bottom, rank + 1, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+class DistStrips:
+    """One strip per rank; `engine` is this rank's strip engine (or any
+    object with the same halo_tensors()/advance_async()/swaps() methods,
+    which the CPU gloo tests use)."""
+
+    def __init__(self, engine, rank: int, world: int, halo_tensors=None, group=None):
+        self.engine, self.rank, self.world, self.group = engine, rank, world, group
+        self._halo = halo_tensors
+
+    def _halos(self):
+        if self._halo is not None:
+            return self._halo()
+        return engine_halo_tensors(self.engine, torch.cuda.current_device())
+
+    def advance_async(self, seed: int, force_thr: int, first_step: int, step_count: int):
+        for s in range(first_step, first_step + step_count):
+            if self.world > 1:
+                exchange_halos(*self._halos(), self.rank, self.world, self.group)
+            self.engine.advance_async(seed, force_thr, s, 1)
+
+    def advance(self, seed: int, force_thr: int, first_step: int, step_count: int) -> int:
+        """Like fhp::advance over the whole lattice: returns the global swap count."""
+        self.engine.swaps(reset=True)
+        self.advance_async(seed, force_thr, first_step, step_count)
+        local = self.engine.swaps()
+        if self.world == 1:
+            return local
+        t = torch.tensor([local], dtype=torch.int64,
+                         device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(t, group=self.group)
+        return int(t.item())
