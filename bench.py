@@ -186,7 +186,8 @@ def main():
     rb, re = strip_rows(H, world)[rank]
     table = P.build_table("fhp3")
     eng = P.Engine(W_LAT, H, rb, re, local)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
     eng.set_table(table)
     eng.init(SEED, DENSITY)

@@ -61,8 +61,8 @@ void fhpg_destroy(fhpg_engine* e);
 /* Thread-local message of the last failure ("" if none). */
 const char* fhpg_last_error(void);
 
-/* Stream all engine work is enqueued on (a cudaStream_t); NULL = the
- * engine's own stream. */
+/* Stream all engine work is enqueued on (a cudaStream_t; NULL = the legacy
+ * default stream). Until this is called the engine uses its own stream. */
 int fhpg_set_stream(fhpg_engine* e, void* cuda_stream);
 
 /* 512-entry collision table, index (chirality << 8) | state

@@ -15,7 +15,7 @@
 struct fhpg_engine {
   int W = 0, H = 0, row_begin = 0, row_end = 0, nrows = 0, device = 0;
   size_t pitch = 0;
-  uint8_t* buf[2] = {nullptr, nullptr};  // (nrows + 2) * pitch each, halo rows included
+  uint8_t* buf[2] = {nullptr, nullptr};  // (nrows + 4) * pitch each: halo, rows, halo, 2 spare
   int cur = 0;
   uint8_t* mask = nullptr;               // nrows * pitch, 0/1
   uint8_t* table = nullptr;              // 512 bytes
@@ -123,7 +123,7 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
     e->nrows = re - rb;
     e->device = device;
     e->pitch = (static_cast<size_t>(W) + 15) / 16 * 16;
-    const size_t bytes = (static_cast<size_t>(e->nrows) + 2) * e->pitch;
+    const size_t bytes = (static_cast<size_t>(e->nrows) + 4) * e->pitch;  // halos + 2 spare rows
     for (int i = 0; i < 2; ++i) {
       ck(cudaMalloc(&e->buf[i], bytes), "cudaMalloc(state)");
       ck(cudaMemset(e->buf[i], 0, bytes), "cudaMemset(state)");
@@ -230,7 +230,7 @@ void fhpg_destroy(fhpg_engine* e) {
 int fhpg_set_stream(fhpg_engine* e, void* s) {
   return guarded([&] {
     need(e);
-    e->stream = s ? static_cast<cudaStream_t>(s) : e->own_stream;
+    e->stream = static_cast<cudaStream_t>(s);  // NULL = the legacy default stream
   });
 }
 

@@ -7,11 +7,12 @@
 
 namespace fhpg {
 
-// Device lattice view of one strip of rows. The buffer holds nrows+2 rows of
+// Device lattice view of one strip of rows. The buffer holds nrows+4 rows of
 // `pitch` bytes: local row -1 (top halo), rows 0..nrows-1 (owned), row nrows
 // (bottom halo). Halo rows are zero where the strip touches the global grid
 // edge (the reference's "out-of-grid rows contribute nothing", step.cpp:47)
-// and hold the neighbour strip's boundary row otherwise. `base` points at
+// and hold the neighbour strip's boundary row otherwise; two spare zero rows
+// follow the bottom halo so the fast path may prefetch past it. `base` points at
 // local row 0, column 0 (reference storage column 1).
 struct StepArgs {
   const uint8_t* src;
@@ -30,8 +31,12 @@ struct StepArgs {
   uint64_t kc_next, kf_next; // step keys of the next step
   int seg_rows;              // rows per warp task (fast path)
   int nbands;                // 512-column bands (fast path)
+  int nbands_groups;         // CTA column groups (fast path)
   int row_lo, row_hi;        // local row range to update, [row_lo, row_hi)
 };
+
+// Fast path launcher (fhpg_step_fast.cu).
+int launch_step_fast(const StepArgs& a, int num_sms, cudaStream_t st);
 
 // Kernel selection for a lattice width.
 bool fast_path_ok(int W);

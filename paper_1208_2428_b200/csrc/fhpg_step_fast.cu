@@ -1,0 +1,440 @@
+// fhpg_step_fast.cu — the hot path: one fused FHP time step for W % 16 == 0.
+//
+// Replaces, per step, sync_ghost_columns (lattice.cpp:32-39), motion_step
+// (step.cpp:40-61, pull offsets backends.cpp:64-73), swap_buffers and
+// collide_rows with its counter-RNG chirality and forcing (step.cpp:63-93).
+//
+// Layout: byte-per-site rows (bit 7 = obstacle, kept in the state; valid
+// tables never change it) in two ping-pong HBM buffers.
+//
+// Work decomposition: one CTA of 32 warps per SM. A warp owns a 512-column
+// band (16 sites per lane: one 128-bit load and one 128-bit store per lane and
+// row) and a segment of rows it streams top to bottom, keeping rows r-1, r,
+// r+1 in registers so every source row is read from HBM once. A CTA covers
+// kBandsPerCta adjacent bands x kSegsPerCta segments.
+//
+// Per row: motion = byte permutes (PRMT, the +-1 column shifts, neighbour
+// lane edge bytes via SHFL) and LOP3 bit-select merges; collision = one LDS
+// per site from a lane-private copy of the LUT (one PRMT forms the address
+// state*256 + lane*4, so lane l always hits bank l). The LUT entry holds the
+// chirality-0 outcome and the XOR to the chirality-1 outcome, whose bit 7
+// flags "depends on chirality". Rows go to a per-warp smem stage.
+//
+// Every kBatch rows the warp resolves the chirality-dependent sites with a
+// load-balanced walk (prefix sum over lanes, each lane takes an equal slice of
+// the batch's dep-site list), evaluating the RNG only there (rng.hpp:25-33;
+// key = per-column key staged in smem + global row) and patching the staged
+// bytes with shared-memory atomics. Forcing (step.cpp:79-88) is resolved the
+// same way on the patched rows. Then the batch leaves with 128-bit streaming
+// stores.
+#include <cstdint>
+#include <type_traits>
+
+#include "fhpg_common.cuh"
+#include "fhpg_kernels.cuh"
+
+namespace fhpg {
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kThreads = 768;
+constexpr int kWarps = kThreads / 32;
+constexpr int kBandsPerCta = 4;
+constexpr int kSegsPerCta = kWarps / kBandsPerCta;
+constexpr int kBatch = 4;
+// Shared memory map (bytes). The LUT uses the first 128 B of every 256-B
+// entry row; the second halves hold the column keys of the CTA's 2048
+// columns (chirality keys in rows 0-127, forcing keys in rows 128-255).
+constexpr int kLutBytes = 256 * 256;
+constexpr int kStageOut = 0;                 // [kBatch][512] bytes
+constexpr int kStageDep = kBatch * 512;      // [kBatch][512] bytes
+constexpr int kStageMask = 2 * kBatch * 512; // [32 lanes][2] u32 dep masks
+constexpr int kWarpStage = 2 * kBatch * 512 + 32 * kBatch * 4;
+constexpr int kSmem = kLutBytes + kWarps * kWarpStage;
+
+template <int B, int E, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v));
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w));
+}
+__device__ __forceinline__ void atoms_xor(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ uint4 ldg128(const uint8_t* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ uint32_t ldg32(const uint8_t* p) {
+  return __ldg(reinterpret_cast<const uint32_t*>(p));
+}
+__device__ __forceinline__ void stg128_cs(uint8_t* p, uint4 v) {
+  __stcs(reinterpret_cast<uint4*>(p), v);
+}
+
+struct Raw {
+  uint4 v;     // this lane's 16 sites
+  uint32_t e;  // lane 0: word left of the band; last lane: word right of it
+};
+
+struct Row {
+  uint32_t w[4];
+  uint32_t L;  // word whose top byte is column x0-1
+  uint32_t R;  // word whose low byte is column x0+16
+};
+
+struct Lane {
+  int lane, last;
+  uint32_t x0;    // first column of the lane (clamped to 0 for inactive lanes)
+  uint32_t eoff;  // column of the edge word this lane loads
+  bool active;
+};
+
+__device__ __forceinline__ Raw load_raw(const uint8_t* row, const Lane& ln) {
+  return Raw{ldg128(row + ln.x0), ldg32(row + ln.eoff)};
+}
+
+__device__ __forceinline__ Row finish(const Raw& r, const Lane& ln) {
+  Row o;
+  o.w[0] = r.v.x;
+  o.w[1] = r.v.y;
+  o.w[2] = r.v.z;
+  o.w[3] = r.v.w;
+  const uint32_t up = __shfl_up_sync(kFull, r.v.w, 1);
+  const uint32_t dn = __shfl_down_sync(kFull, r.v.x, 1);
+  o.L = ln.lane == 0 ? r.e : up;
+  o.R = ln.lane == ln.last ? r.e : dn;
+  return o;
+}
+
+// Column x-1 / x+1 at every byte of word j.
+__device__ __forceinline__ uint32_t shl1(const Row& r, int j) {
+  return __byte_perm(j == 0 ? r.L : r.w[j - 1], r.w[j], 0x6543);
+}
+__device__ __forceinline__ uint32_t shr1(const Row& r, int j) {
+  return __byte_perm(r.w[j], j == 3 ? r.R : r.w[j + 1], 0x4321);
+}
+// (a & m) | (b & ~m)
+__device__ __forceinline__ uint32_t mux(uint32_t a, uint32_t b, uint32_t m) {
+  return (a & m) | (b & ~m);
+}
+
+// One destination row. Pull sources (backends.cpp:64-73): k0 (x+q, r+1),
+// k1 (x+q-1, r+1), k2 (x-1, r), k3 (x+q-1, r-1), k4 (x+q, r-1), k5 (x+1, r);
+// rest bit stays, bit 7 = own obstacle bit. Returns the packed dep-site mask
+// (bit 8b + 7 - j <-> byte b of word j).
+template <int Q>
+__device__ __forceinline__ uint32_t row_update(const Row& P, const Row& C, const Row& N,
+                                               uint32_t lut, uint32_t laneoff, uint32_t out0[4],
+                                               uint32_t dep[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t n0 = Q ? shr1(N, j) : N.w[j];
+    const uint32_t n1 = Q ? N.w[j] : shl1(N, j);
+    const uint32_t p3 = Q ? P.w[j] : shl1(P, j);
+    const uint32_t p4 = Q ? shr1(P, j) : P.w[j];
+    uint32_t m = mux(C.w[j], n0, 0xC0C0C0C0u);  // bit 0 correct, 1-5 overwritten below
+    m = mux(n1, m, 0x02020202u);
+    m = mux(shl1(C, j), m, 0x04040404u);
+    m = mux(p3, m, 0x08080808u);
+    m = mux(p4, m, 0x10101010u);
+    m = mux(shr1(C, j), m, 0x20202020u);
+    // [laneoff.b0 (= lane*4), m.bk, 0, 0] -> state * 256 + lane * 4
+    const uint32_t v0 = lds32(lut + __byte_perm(laneoff, m, 0x1140));
+    const uint32_t v1 = lds32(lut + __byte_perm(laneoff, m, 0x1150));
+    const uint32_t v2 = lds32(lut + __byte_perm(laneoff, m, 0x1160));
+    const uint32_t v3 = lds32(lut + __byte_perm(laneoff, m, 0x1170));
+    const uint32_t A = __byte_perm(v0, v1, 0x5140);
+    const uint32_t B = __byte_perm(v2, v3, 0x5140);
+    out0[j] = __byte_perm(A, B, 0x5410);
+    dep[j] = __byte_perm(A, B, 0x7632);
+  }
+  const uint32_t K = 0x80808080u;
+  return (dep[0] & K) | ((dep[1] >> 1) & (K >> 1)) | ((dep[2] >> 2) & (K >> 2)) |
+         ((dep[3] >> 3) & (K >> 3));
+}
+
+// One dep site handed to a walk callback.
+struct Site {
+  uint32_t row;   // row inside the batch
+  uint32_t j4;    // 4 * word index inside the owner lane's 16 bytes
+  uint32_t sh;    // 8 * byte index inside that word
+  uint32_t key;   // smem address of the site's column key
+  uint32_t word;  // smem address of the site's staged out word
+};
+
+// Load-balanced walk over the dep sites of a batch. Each lane holds two
+// masks: M01 = rows 0/1 and M23 = rows 2/3 (row 2k in the high nibbles of the
+// bytes, bit 8b+7-j; row 2k+1 in the low nibbles, bit 8b+3-j). The sites are
+// numbered lane-major; every lane takes an equal contiguous slice of that
+// list (prefix sum + binary search over lanes) and calls fn(site) for each.
+template <typename Fn>
+__device__ __forceinline__ void warp_walk(uint32_t M01, uint32_t M23, uint32_t smask,
+                                          uint32_t stage, uint32_t keys, int lane, Fn&& fn) {
+  const int cnt = __popc(M01) + __popc(M23);
+  int incl = cnt;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const int T = __shfl_sync(kFull, incl, 31);
+  if (T == 0) return;
+  asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(smask + lane * 8), "r"(M01), "r"(M23));
+  const int s = (lane * T) >> 5;
+  const int e = ((lane + 1) * T) >> 5;
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step; step >>= 1) {
+    const int v = __shfl_sync(kFull, incl, o + step - 1);
+    if (v <= s) o += step;
+  }
+  const int excl_o = __shfl_sync(kFull, incl - cnt, o);
+  __syncwarp();
+  if (s < e) {
+    int k = s - excl_o;
+    uint32_t off = static_cast<uint32_t>(o) * 8u;  // byte offset of the current mask
+    uint32_t mask = lds32(smask + off);
+    for (;;) {
+      const int c = __popc(mask);
+      if (k < c) break;
+      k -= c;
+      off += 4u;
+      mask = lds32(smask + off);
+    }
+    for (; k > 0; --k) mask ^= 0x80000000u >> __clz(mask);
+    for (int it = s; it < e; ++it) {
+      while (mask == 0u) {
+        off += 4u;
+        mask = lds32(smask + off);
+      }
+      const uint32_t q = __clz(mask);
+      mask ^= 0x80000000u >> q;
+      Site t;
+      t.row = ((off >> 1) & 2u) | ((q >> 2) & 1u);
+      t.j4 = (q & 3u) << 2;
+      t.sh = (q & 0x18u) ^ 0x18u;
+      t.key = keys + (off >> 3) * 256u + (t.j4 + (t.sh >> 3)) * 8u;
+      t.word = stage + t.row * 512u + (off >> 3) * 16u + t.j4;
+      fn(t);
+    }
+  }
+  __syncwarp();
+}
+
+template <int P0, bool FORCE, bool FULL>
+__device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint32_t keys,
+                                          uint32_t stage, const Lane& ln, int rb, int nb,
+                                          Row (&win)[kBatch + 2], Raw (&pre)[2],
+                                          const uint8_t*& nxt, uint8_t*& out, unsigned& swaps) {
+  const size_t pitch = a.pitch;
+  const uint32_t smask = stage + kStageMask;
+  const uint32_t my = stage + ln.lane * 16;  // this lane's 16 bytes of a staged row
+  const uint32_t laneoff = ln.lane * 4u;
+  uint32_t F[kBatch];
+  static_for<0, kBatch>([&](auto ic) {
+    constexpr int i = decltype(ic)::value;
+    F[i] = 0u;
+    if (FULL || i < nb) {
+      win[i + 2] = finish(pre[i & 1], ln);
+      pre[i & 1] = load_raw(nxt, ln);
+      nxt += pitch;
+      uint32_t o[4], d[4];
+      F[i] = row_update<(P0 + i) & 1>(win[i], win[i + 1], win[i + 2], lut, laneoff, o, d);
+      sts128(my + i * 512, o[0], o[1], o[2], o[3]);
+      sts128(my + kStageDep + i * 512, d[0], d[1], d[2], d[3]);
+    }
+  });
+  uint32_t M01 = F[0] | (F[1] >> 4), M23 = F[2] | (F[3] >> 4);
+  if (!ln.active) M01 = M23 = 0u;
+  __syncwarp();
+  const uint64_t ybase = static_cast<uint64_t>(a.row0 + rb);
+  // Chirality: sites whose two outcomes differ (rng.hpp:25-33 keyed by the
+  // 1-based storage column and global row, step.cpp:73-76).
+  warp_walk(M01, M23, smask, stage, keys, ln.lane, [&](const Site& t) {
+    const uint32_t chir = fin64_bit0(lds64(t.key) + ybase + t.row);
+    const uint32_t d = lds32(t.word + kStageDep) & (0x7Fu << t.sh);
+    atoms_xor(t.word, chir ? d : 0u);
+  });
+  if (FORCE) {
+    // Forcing on the post-collision state (step.cpp:79-88): fluid, W set, E clear.
+    uint32_t G[kBatch];
+    static_for<0, kBatch>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      G[i] = 0u;
+      if (FULL || i < nb) {
+        const uint4 f = lds128(my + i * 512);
+        const uint32_t w[4] = {f.x, f.y, f.z, f.w};
+        uint32_t g = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          g |= (((w[j] >> 5) & ~(w[j] >> 2) & ~(w[j] >> 7)) & 0x01010101u) << (7 - j);
+        G[i] = g;
+      }
+    });
+    uint32_t G01 = G[0] | (G[1] >> 4), G23 = G[2] | (G[3] >> 4);
+    if (!ln.active) G01 = G23 = 0u;
+    warp_walk(G01, G23, smask, stage, keys + 128u * 256u, ln.lane, [&](const Site& t) {
+      if ((fin64(lds64(t.key) + ybase + t.row) >> 32) < a.thr) {
+        atoms_xor(t.word, 0x24u << t.sh);
+        ++swaps;
+      }
+    });
+  }
+  static_for<0, kBatch>([&](auto ic) {
+    constexpr int i = decltype(ic)::value;
+    if ((FULL || i < nb) && ln.active) stg128_cs(out + i * pitch, lds128(my + i * 512));
+  });
+  out += kBatch * pitch;
+  // The window of the next batch: rows rb+3, rb+4.
+  win[0] = win[kBatch];
+  win[1] = win[kBatch + 1];
+  __syncwarp();
+}
+
+template <int P0, bool FORCE>
+__device__ __forceinline__ void run_segment(const StepArgs& a, uint32_t lut, uint32_t keys,
+                                            uint32_t stage, const Lane& ln, int r_begin,
+                                            int r_end, unsigned& swaps) {
+  const size_t pitch = a.pitch;
+  Row win[kBatch + 2];  // rows rb-1 .. rb+kBatch
+  win[0] = finish(load_raw(a.src + (r_begin - 1) * (long long)pitch, ln), ln);
+  win[1] = finish(load_raw(a.src + r_begin * (long long)pitch, ln), ln);
+  const uint8_t* nxt = a.src + (r_begin + 1) * (long long)pitch;
+  Raw pre[2];
+  pre[0] = load_raw(nxt, ln);
+  nxt += pitch;
+  pre[1] = load_raw(nxt, ln);
+  nxt += pitch;  // buffers carry 2 spare zero rows below the halo: over-prefetch is safe
+  uint8_t* out = a.dst + r_begin * (long long)pitch + ln.x0;
+  int rb = r_begin;
+  for (; rb + kBatch <= r_end; rb += kBatch)
+    run_batch<P0, FORCE, true>(a, lut, keys, stage, ln, rb, kBatch, win, pre, nxt, out, swaps);
+  if (rb < r_end)
+    run_batch<P0, FORCE, false>(a, lut, keys, stage, ln, rb, r_end - rb, win, pre, nxt, out, swaps);
+}
+
+template <bool FORCE>
+__global__ void __launch_bounds__(kThreads, 1) step_fast_kernel(StepArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  const int warp = threadIdx.x >> 5;
+  const int band_group = blockIdx.x % a.nbands_groups;
+  const int seg_group = blockIdx.x / a.nbands_groups;
+  const int cta_x0 = band_group * kBandsPerCta * 512;
+  // LUT: lane-private words (e*256 + 4l) = out(ch0) | flagged XOR(ch0, ch1) << 8.
+  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+    const int e = i >> 5, l = i & 31;
+    const uint32_t o0 = a.table[e], o1 = a.table[256 + e];
+    const uint32_t x = o0 ^ o1;
+    sts32(sbase + e * 256 + l * 4, o0 | ((x | (x ? 0x80u : 0u)) << 8));
+  }
+  // Column keys of this CTA's 2048 columns into the LUT rows' second halves:
+  // column c at row c >> 4, +128 + (c & 15) * 8 (a lane's 16 keys share a
+  // row); forcing keys 128 rows further.
+  for (int c = threadIdx.x; c < kBandsPerCta * 512; c += blockDim.x) {
+    const int x = cta_x0 + c;
+    if (x < a.W) {
+      sts64(sbase + (c >> 4) * 256 + 128 + (c & 15) * 8, a.zc[x]);
+      if (FORCE) sts64(sbase + (128 + (c >> 4)) * 256 + 128 + (c & 15) * 8, a.zf[x]);
+    }
+  }
+  __syncthreads();
+  // Next step's column keys (read by the next launch only).
+  if (a.zc_next) {
+    const int n = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.W; i += n) {
+      a.zc_next[i] = column_key(a.kc_next, static_cast<uint64_t>(i) + 1);
+      if (a.zf_next) a.zf_next[i] = column_key(a.kf_next, static_cast<uint64_t>(i) + 1);
+    }
+  }
+
+  const int bic = warp % kBandsPerCta;
+  const int band = band_group * kBandsPerCta + bic;
+  const int seg = seg_group * kSegsPerCta + warp / kBandsPerCta;
+  const int r_begin = a.row_lo + seg * a.seg_rows;
+  if (band >= a.nbands || r_begin >= a.row_hi) return;  // whole warp
+  const int r_end = min(a.row_hi, r_begin + a.seg_rows);
+
+  Lane ln;
+  ln.lane = threadIdx.x & 31;
+  const int band_x = band * 512;
+  const int x0 = band_x + ln.lane * 16;
+  ln.active = x0 < a.W;
+  ln.x0 = ln.active ? x0 : 0;
+  ln.last = min(31, (a.W - band_x) / 16 - 1);
+  ln.eoff = ln.lane == 0 ? (x0 == 0 ? a.W - 4 : x0 - 4)
+                         : (ln.lane == ln.last ? (x0 + 16 == a.W ? 0 : x0 + 16) : ln.x0);
+  const uint32_t lut = sbase;
+  const uint32_t keys = sbase + bic * 32 * 256 + 128;  // a band's 512 keys: 32 LUT rows
+  const uint32_t stage = sbase + kLutBytes + warp * kWarpStage;
+  unsigned swaps = 0;
+  if ((a.row0 + r_begin) & 1)
+    run_segment<1, FORCE>(a, lut, keys, stage, ln, r_begin, r_end, swaps);
+  else
+    run_segment<0, FORCE>(a, lut, keys, stage, ln, r_begin, r_end, swaps);
+
+  if (FORCE) {
+    unsigned long long s = swaps;
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+    if (ln.lane == 0 && s) atomicAdd(a.swaps, s);
+  }
+}
+
+}  // namespace
+
+int launch_step_fast(const StepArgs& a0, int num_sms, cudaStream_t st) {
+  StepArgs a = a0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(step_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(step_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr_set = true;
+  }
+  const int rows = a.row_hi - a.row_lo;
+  a.nbands = (a.W + 511) / 512;
+  a.nbands_groups = (a.nbands + kBandsPerCta - 1) / kBandsPerCta;
+  // One wave: at most num_sms CTAs (one per SM), each kSegsPerCta segments deep.
+  int seg_groups = num_sms / a.nbands_groups;
+  if (seg_groups < 1) seg_groups = 1;
+  int seg = (rows + seg_groups * kSegsPerCta - 1) / (seg_groups * kSegsPerCta);
+  if (seg < 8) seg = 8;
+  a.seg_rows = seg;
+  const int nseg = (rows + seg - 1) / seg;
+  seg_groups = (nseg + kSegsPerCta - 1) / kSegsPerCta;
+  const int grid = a.nbands_groups * seg_groups;
+  if (a.thr != 0) step_fast_kernel<true><<<grid, kThreads, kSmem, st>>>(a);
+  else step_fast_kernel<false><<<grid, kThreads, kSmem, st>>>(a);
+  return 1;
+}
+
+}  // namespace fhpg
