@@ -17,8 +17,10 @@
 // lane edge bytes via SHFL) and LOP3 bit-select merges; collision = one LDS
 // per site from a lane-private copy of the LUT (one PRMT forms the address
 // state*256 + lane*4, so lane l always hits bank l). The LUT entry holds the
-// chirality-0 outcome and the XOR to the chirality-1 outcome, whose bit 7
-// flags "depends on chirality". Rows go to a per-warp smem stage.
+// chirality-0 outcome (byte 0) and the XOR to the chirality-1 outcome (byte
+// 2), whose bit 7 flags "depends on chirality". Rows go to a per-warp smem
+// stage. Byte moves that would be ALU shifts are written as multiplies (FMA
+// pipe) because the ALU pipe is the binding resource.
 //
 // Every kBatch rows the warp resolves the chirality-dependent sites with a
 // load-balanced walk (prefix sum over lanes, each lane takes an equal slice of
@@ -37,7 +39,7 @@ namespace fhpg {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kThreads = 768;
+constexpr int kThreads = 640;
 constexpr int kWarps = kThreads / 32;
 constexpr int kBandsPerCta = 4;
 constexpr int kSegsPerCta = kWarps / kBandsPerCta;
@@ -112,6 +114,10 @@ struct Row {
   uint32_t R;  // word whose low byte is column x0+16
 };
 
+struct Konst {  // run-time copies of StepArgs::k16 / k256 / k2p24
+  uint32_t k16, k256, k2p24;
+};
+
 struct Lane {
   int lane, last;
   uint32_t x0;    // first column of the lane (clamped to 0 for inactive lanes)
@@ -143,9 +149,13 @@ __device__ __forceinline__ uint32_t shl1(const Row& r, int j) {
 __device__ __forceinline__ uint32_t shr1(const Row& r, int j) {
   return __byte_perm(r.w[j], j == 3 ? r.R : r.w[j + 1], 0x4321);
 }
-// (a & m) | (b & ~m)
-__device__ __forceinline__ uint32_t mux(uint32_t a, uint32_t b, uint32_t m) {
-  return (a & m) | (b & ~m);
+// (a & m) | (b & ~m) as one LOP3 (the compiler otherwise splits the chain
+// into AND + OR-AND pairs).
+template <uint32_t M>
+__device__ __forceinline__ uint32_t mux(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "n"(M));
+  return d;
 }
 
 // One destination row. Pull sources (backends.cpp:64-73): k0 (x+q, r+1),
@@ -154,7 +164,8 @@ __device__ __forceinline__ uint32_t mux(uint32_t a, uint32_t b, uint32_t m) {
 // (bit 8b + 7 - j <-> byte b of word j).
 template <int Q>
 __device__ __forceinline__ uint32_t row_update(const Row& P, const Row& C, const Row& N,
-                                               uint32_t lut, uint32_t laneoff, uint32_t out0[4],
+                                               uint32_t lut, uint32_t laneoff, const Konst& K,
+                                               uint32_t out0[4],
                                                uint32_t dep[4]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -162,41 +173,56 @@ __device__ __forceinline__ uint32_t row_update(const Row& P, const Row& C, const
     const uint32_t n1 = Q ? N.w[j] : shl1(N, j);
     const uint32_t p3 = Q ? P.w[j] : shl1(P, j);
     const uint32_t p4 = Q ? shr1(P, j) : P.w[j];
-    uint32_t m = mux(C.w[j], n0, 0xC0C0C0C0u);  // bit 0 correct, 1-5 overwritten below
-    m = mux(n1, m, 0x02020202u);
-    m = mux(shl1(C, j), m, 0x04040404u);
-    m = mux(p3, m, 0x08080808u);
-    m = mux(p4, m, 0x10101010u);
-    m = mux(shr1(C, j), m, 0x20202020u);
+    uint32_t m = mux<0xC0C0C0C0u>(C.w[j], n0);  // bit 0 correct, 1-5 overwritten below
+    m = mux<0x02020202u>(n1, m);
+    m = mux<0x04040404u>(shl1(C, j), m);
+    m = mux<0x08080808u>(p3, m);
+    m = mux<0x10101010u>(p4, m);
+    m = mux<0x20202020u>(shr1(C, j), m);
     // [laneoff.b0 (= lane*4), m.bk, 0, 0] -> state * 256 + lane * 4
     const uint32_t v0 = lds32(lut + __byte_perm(laneoff, m, 0x1140));
     const uint32_t v1 = lds32(lut + __byte_perm(laneoff, m, 0x1150));
     const uint32_t v2 = lds32(lut + __byte_perm(laneoff, m, 0x1160));
     const uint32_t v3 = lds32(lut + __byte_perm(laneoff, m, 0x1170));
-    const uint32_t A = __byte_perm(v0, v1, 0x5140);
-    const uint32_t B = __byte_perm(v2, v3, 0x5140);
+    // Entries are out | xor << 16 with both < 256, so v0 + 256 v1 packs
+    // [out_0, out_1, xor_0, xor_1] without carries (IMAD on the FMA pipe).
+    const uint32_t A = v1 * K.k256 + v0;
+    const uint32_t B = v3 * K.k256 + v2;
     out0[j] = __byte_perm(A, B, 0x5410);
     dep[j] = __byte_perm(A, B, 0x7632);
   }
-  const uint32_t K = 0x80808080u;
-  return (dep[0] & K) | ((dep[1] >> 1) & (K >> 1)) | ((dep[2] >> 2) & (K >> 2)) |
-         ((dep[3] >> 3) & (K >> 3));
+  // 16-bit dep mask, bit 4j + b <-> byte b of word j: one multiply gathers
+  // the four flag bits (bit 7 of each byte) into bits 28..31, a high
+  // multiply extracts that nibble, a multiply-add places it.
+  uint32_t f = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t nib = __umulhi((dep[j] & 0x80808080u) * 0x00204081u, K.k16);
+    f = nib * (1u << (4 * j)) + f;
+  }
+  return f;
 }
 
 // One dep site handed to a walk callback.
 struct Site {
   uint32_t row;   // row inside the batch
-  uint32_t j4;    // 4 * word index inside the owner lane's 16 bytes
-  uint32_t sh;    // 8 * byte index inside that word
+  uint32_t sh;    // 8 * byte index inside the staged word
   uint32_t key;   // smem address of the site's column key
   uint32_t word;  // smem address of the site's staged out word
 };
 
+// Bit index of the highest set bit (PTX bfind: one FLO).
+__device__ __forceinline__ uint32_t top_bit(uint32_t m) {
+  uint32_t p;
+  asm("bfind.u32 %0, %1;" : "=r"(p) : "r"(m));
+  return p;
+}
+
 // Load-balanced walk over the dep sites of a batch. Each lane holds two
-// masks: M01 = rows 0/1 and M23 = rows 2/3 (row 2k in the high nibbles of the
-// bytes, bit 8b+7-j; row 2k+1 in the low nibbles, bit 8b+3-j). The sites are
-// numbered lane-major; every lane takes an equal contiguous slice of that
-// list (prefix sum + binary search over lanes) and calls fn(site) for each.
+// masks, M01 (rows 0, 1) and M23 (rows 2, 3): bit 16*r' + c <-> row 2k+r',
+// column c of the lane's 16. The sites are numbered lane-major; every lane
+// takes an equal contiguous slice of that list (prefix sum + binary search
+// over lanes) and calls fn(site) for each.
 template <typename Fn>
 __device__ __forceinline__ void warp_walk(uint32_t M01, uint32_t M23, uint32_t smask,
                                           uint32_t stage, uint32_t keys, int lane, Fn&& fn) {
@@ -231,20 +257,27 @@ __device__ __forceinline__ void warp_walk(uint32_t M01, uint32_t M23, uint32_t s
       off += 4u;
       mask = lds32(smask + off);
     }
-    for (; k > 0; --k) mask ^= 0x80000000u >> __clz(mask);
+    for (; k > 0; --k) mask ^= 1u << top_bit(mask);
+    // Per-owner bases, refreshed when the walk moves to the next mask.
+    uint32_t kbase = keys + (off >> 3) * 256u;
+    uint32_t wbase = stage + (off >> 3) * 16u + (off & 4u) * 256u;
+    uint32_t rbase = (off >> 1) & 2u;
     for (int it = s; it < e; ++it) {
       while (mask == 0u) {
         off += 4u;
         mask = lds32(smask + off);
+        kbase = keys + (off >> 3) * 256u;
+        wbase = stage + (off >> 3) * 16u + (off & 4u) * 256u;
+        rbase = (off >> 1) & 2u;
       }
-      const uint32_t q = __clz(mask);
-      mask ^= 0x80000000u >> q;
+      const uint32_t p = top_bit(mask);
+      mask ^= 1u << p;
+      const uint32_t r1 = p >> 4;  // second row of the pair
       Site t;
-      t.row = ((off >> 1) & 2u) | ((q >> 2) & 1u);
-      t.j4 = (q & 3u) << 2;
-      t.sh = (q & 0x18u) ^ 0x18u;
-      t.key = keys + (off >> 3) * 256u + (t.j4 + (t.sh >> 3)) * 8u;
-      t.word = stage + t.row * 512u + (off >> 3) * 16u + t.j4;
+      t.row = rbase + r1;
+      t.sh = (p & 3u) * 8u;
+      t.key = kbase + (p & 15u) * 8u;
+      t.word = wbase + r1 * 512u + (p & 12u);
       fn(t);
     }
   }
@@ -260,6 +293,7 @@ __device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint3
   const uint32_t smask = stage + kStageMask;
   const uint32_t my = stage + ln.lane * 16;  // this lane's 16 bytes of a staged row
   const uint32_t laneoff = ln.lane * 4u;
+  const Konst K{a.k16, a.k256, a.k2p24};
   uint32_t F[kBatch];
   static_for<0, kBatch>([&](auto ic) {
     constexpr int i = decltype(ic)::value;
@@ -269,12 +303,12 @@ __device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint3
       pre[i & 1] = load_raw(nxt, ln);
       nxt += pitch;
       uint32_t o[4], d[4];
-      F[i] = row_update<(P0 + i) & 1>(win[i], win[i + 1], win[i + 2], lut, laneoff, o, d);
+      F[i] = row_update<(P0 + i) & 1>(win[i], win[i + 1], win[i + 2], lut, laneoff, K, o, d);
       sts128(my + i * 512, o[0], o[1], o[2], o[3]);
       sts128(my + kStageDep + i * 512, d[0], d[1], d[2], d[3]);
     }
   });
-  uint32_t M01 = F[0] | (F[1] >> 4), M23 = F[2] | (F[3] >> 4);
+  uint32_t M01 = F[1] * 65536u + F[0], M23 = F[3] * 65536u + F[2];
   if (!ln.active) M01 = M23 = 0u;
   __syncwarp();
   const uint64_t ybase = static_cast<uint64_t>(a.row0 + rb);
@@ -297,11 +331,12 @@ __device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint3
         uint32_t g = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          g |= (((w[j] >> 5) & ~(w[j] >> 2) & ~(w[j] >> 7)) & 0x01010101u) << (7 - j);
+          g = __umulhi((((w[j] >> 5) & ~(w[j] >> 2) & ~(w[j] >> 7)) & 0x01010101u) * 0x10204080u,
+                       K.k16) * (1u << (4 * j)) + g;
         G[i] = g;
       }
     });
-    uint32_t G01 = G[0] | (G[1] >> 4), G23 = G[2] | (G[3] >> 4);
+    uint32_t G01 = G[1] * 65536u + G[0], G23 = G[3] * 65536u + G[2];
     if (!ln.active) G01 = G23 = 0u;
     warp_walk(G01, G23, smask, stage, keys + 128u * 256u, ln.lane, [&](const Site& t) {
       if ((fin64(lds64(t.key) + ybase + t.row) >> 32) < a.thr) {
@@ -351,12 +386,12 @@ __global__ void __launch_bounds__(kThreads, 1) step_fast_kernel(StepArgs a) {
   const int band_group = blockIdx.x % a.nbands_groups;
   const int seg_group = blockIdx.x / a.nbands_groups;
   const int cta_x0 = band_group * kBandsPerCta * 512;
-  // LUT: lane-private words (e*256 + 4l) = out(ch0) | flagged XOR(ch0, ch1) << 8.
+  // LUT: lane-private words (e*256 + 4l) = out(ch0) | flagged XOR(ch0, ch1) << 16.
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     const int e = i >> 5, l = i & 31;
     const uint32_t o0 = a.table[e], o1 = a.table[256 + e];
     const uint32_t x = o0 ^ o1;
-    sts32(sbase + e * 256 + l * 4, o0 | ((x | (x ? 0x80u : 0u)) << 8));
+    sts32(sbase + e * 256 + l * 4, o0 | ((x | (x ? 0x80u : 0u)) << 16));
   }
   // Column keys of this CTA's 2048 columns into the LUT rows' second halves:
   // column c at row c >> 4, +128 + (c & 15) * 8 (a lane's 16 keys share a
@@ -421,6 +456,9 @@ int launch_step_fast(const StepArgs& a0, int num_sms, cudaStream_t st) {
     attr_set = true;
   }
   const int rows = a.row_hi - a.row_lo;
+  a.k16 = 16u;
+  a.k256 = 256u;
+  a.k2p24 = 1u << 24;
   a.nbands = (a.W + 511) / 512;
   a.nbands_groups = (a.nbands + kBandsPerCta - 1) / kBandsPerCta;
   // One wave: at most num_sms CTAs (one per SM), each kSegsPerCta segments deep.
