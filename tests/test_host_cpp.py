@@ -89,7 +89,8 @@ def test_cli_run_matches_reference_digest(tmp_path, golden):
         prof = (tmp_path / f"o_step{step}_profile.csv").read_text().splitlines()
         assert prof[0] == "row,mean_ux,sample_count" and len(prof) == 1 + 31
         pgm = (tmp_path / f"o_step{step}_density.pgm").read_bytes()
-        assert pgm.startswith(b"P5\n12 8\n255\n") and len(pgm) == 11 + 96
+        hdr = b"P5\n12 8\n255\n"
+        assert pgm.startswith(hdr) and len(pgm) == len(hdr) + 96
 
 
 @pytest.mark.gpu
