@@ -317,3 +317,42 @@ void fo_cylinder(int W, int H, double cx, double cy, double R, uint8_t* mask) {
       mask[(size_t)r * W + (x - 1)] = (uint8_t)(px * px + py * py <= R * R);
     }
 }
+
+/* One step of a row strip, for the multi-process decomposition tests: the
+ * strip owns global rows [row0, row0+nrows) of a W x H lattice; `src` holds
+ * nrows+2 rows (halo row above, owned rows, halo row below; halos are zero
+ * where the strip touches the grid edge), `mask` the owned rows' obstacle
+ * bytes. Writes the owned rows after motion + collision + forcing of global
+ * step `step` into `dst` (nrows rows). Same rules as fo_advance with the RNG
+ * keyed by the global row. Returns the accepted swaps. */
+uint64_t fo_step_strip(int W, int H, int row0, int nrows, const uint8_t* src, const uint8_t* mask,
+                       const uint8_t* table, uint64_t seed, uint64_t thr, uint64_t step,
+                       uint8_t* dst) {
+  (void)H;
+  uint64_t swaps = 0;
+  for (int lr = 0; lr < nrows; ++lr) {
+    const int r = row0 + lr;
+    int dx[6];
+    pull_dx(r & 1, dx);
+    for (int x = 0; x < W; ++x) {
+      const uint8_t* c = src + (size_t)(lr + 1) * W; /* row r in the halo-extended buffer */
+      unsigned v = c[x] & 0x40u;
+      for (int k = 0; k < 6; ++k) {
+        const uint8_t* s = src + (size_t)(lr + 1 + kPullDr[k]) * W;
+        const int sx = ((x + dx[k]) % W + W) % W;
+        v |= s[sx] & (1u << k);
+      }
+      if (mask[(size_t)lr * W + x]) v |= 0x80u;
+      const unsigned ch =
+          (unsigned)(fo_node_random(seed, 2, step, (uint64_t)x + 1, (uint64_t)r) & 1u);
+      unsigned out = table[(ch << 8) | v];
+      if (!(out & 0x80u) && (out & 0x20u) && !(out & 0x04u) &&
+          fo_bernoulli(fo_node_random(seed, 1, step, (uint64_t)x + 1, (uint64_t)r), thr)) {
+        out = (out & ~0x20u) | 0x04u;
+        ++swaps;
+      }
+      dst[(size_t)lr * W + x] = (uint8_t)out;
+    }
+  }
+  return swaps;
+}

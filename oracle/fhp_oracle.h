@@ -25,6 +25,9 @@ void fo_cells(int W, int H, const uint8_t* state, int B, int32_t* nodes, int32_t
 void fo_rows(int W, int H, const uint8_t* state, int64_t* px, int32_t* fluid);
 void fo_scramble(int W, int H, uint64_t seed, uint8_t* state, uint8_t* mask);
 void fo_cylinder(int W, int H, double cx, double cy, double R, uint8_t* mask);
+uint64_t fo_step_strip(int W, int H, int row0, int nrows, const uint8_t* src, const uint8_t* mask,
+                       const uint8_t* table, uint64_t seed, uint64_t thr, uint64_t step,
+                       uint8_t* dst);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,9 @@ class Port:
         L.fo_rows.argtypes = [C.c_int, C.c_int, u8p, i64p, i32p]
         L.fo_scramble.argtypes = [C.c_int, C.c_int, C.c_uint64, u8p, u8p]
         L.fo_cylinder.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, u8p]
+        L.fo_step_strip.restype = C.c_uint64
+        L.fo_step_strip.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, u8p, u8p, u8p, C.c_uint64,
+                                    C.c_uint64, C.c_uint64, u8p]
 
     def mix64(self, z):
         return self.lib.fo_mix64(z)
@@ -140,6 +143,15 @@ class Port:
         m = np.zeros((H, W), np.uint8)
         self.lib.fo_cylinder(W, H, cx, cy, R, _ptr(m))
         return m
+
+    def step_strip(self, H, row0, src_with_halos, mask, table, seed, thr, step):
+        """One step of a row strip (fo_step_strip). src_with_halos: (nrows+2, W)."""
+        src = _u8(src_with_halos)
+        nrows, W = src.shape[0] - 2, src.shape[1]
+        dst = np.zeros((nrows, W), np.uint8)
+        sw = self.lib.fo_step_strip(W, H, row0, nrows, _ptr(src), _ptr(_u8(mask)), _ptr(_u8(table)),
+                                    seed, thr, step, _ptr(dst))
+        return dst, sw
 
     def rows(self, state):
         s = _u8(state)

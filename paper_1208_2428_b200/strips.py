@@ -69,6 +69,70 @@ def exchange_halos(send_top, send_bottom, recv_top, recv_bottom, rank: int, worl
             req.wait()
 
 
+class LocalStrips:
+    """Several strip engines driven from one process (one GPU each, or all on
+    one GPU to exercise the decomposition): halo rows are moved with
+    device-to-device copies ordered on one shared stream before every step."""
+
+    def __init__(self, width: int, height: int, n: int, devices=None):
+        from .engine import Engine
+        self.W, self.H = width, height
+        self.rows = strip_rows(height, n)
+        self.devices = list(devices) if devices is not None else [0] * n
+        self.engines = [Engine(width, height, rb, re, dev)
+                        for (rb, re), dev in zip(self.rows, self.devices)]
+        self.streams = {}
+        for e, dev in zip(self.engines, self.devices):
+            if dev not in self.streams:
+                self.streams[dev] = torch.cuda.Stream(device=dev)
+            e.set_stream(self.streams[dev].cuda_stream)
+
+    def set_table(self, table):
+        for e in self.engines:
+            e.set_table(table)
+
+    def set_obstacles(self, mask):
+        for e, (rb, re) in zip(self.engines, self.rows):
+            e.set_obstacles(mask[rb:re])
+
+    def upload(self, state):
+        for e, (rb, re) in zip(self.engines, self.rows):
+            e.upload(state[rb:re])
+
+    def init(self, seed: int, density: float):
+        for e in self.engines:
+            e.init(seed, density)
+
+    def download(self):
+        import numpy as np
+        return np.concatenate([e.download() for e in self.engines], axis=0)
+
+    def _exchange(self):
+        halos = [engine_halo_tensors(e, dev) for e, dev in zip(self.engines, self.devices)]
+        for i in range(len(self.engines) - 1):
+            up, dn = halos[i], halos[i + 1]
+            # strip i's last row -> halo above strip i+1, and back.
+            with torch.cuda.stream(self.streams[self.devices[i + 1]]):
+                dn[2].copy_(up[1], non_blocking=True)
+            with torch.cuda.stream(self.streams[self.devices[i]]):
+                up[3].copy_(dn[0], non_blocking=True)
+        if len(self.streams) > 1:  # cross-device copies: fence all streams
+            for s in self.streams.values():
+                s.synchronize()
+
+    def advance(self, seed: int, force_p: float, first_step: int, step_count: int) -> int:
+        from .engine import bernoulli_threshold
+        thr = bernoulli_threshold(force_p)
+        for e in self.engines:
+            e.swaps(reset=True)
+        for s in range(first_step, first_step + step_count):
+            if len(self.engines) > 1:
+                self._exchange()
+            for e in self.engines:
+                e.advance_async(seed, thr, s, 1)
+        return sum(e.swaps() for e in self.engines)
+
+
 class DistStrips:
     """One strip per rank; `engine` is this rank's strip engine (or any
     object with the same halo_tensors()/advance_async()/swaps() methods,
