@@ -148,6 +148,9 @@ class DistStrips:
         return engine_halo_tensors(self.engine, torch.cuda.current_device())
 
     def advance_async(self, seed: int, force_thr: int, first_step: int, step_count: int):
+        if self.world == 1:  # no exchange: one call, the step kernels chain the column keys
+            self.engine.advance_async(seed, force_thr, first_step, step_count)
+            return
         for s in range(first_step, first_step + step_count):
             if self.world > 1:
                 exchange_halos(*self._halos(), self.rank, self.world, self.group)
