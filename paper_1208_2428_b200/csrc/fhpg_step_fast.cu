@@ -52,7 +52,9 @@ constexpr int kStageOut = 0;                 // [kBatch][512] bytes
 constexpr int kStageDep = kBatch * 512;      // [kBatch][512] bytes
 constexpr int kStageMask = 2 * kBatch * 512; // [32 lanes][2] u32 dep masks
 constexpr int kWarpStage = 2 * kBatch * 512 + 32 * kBatch * 4;
-constexpr int kSmem = kLutBytes + kWarps * kWarpStage;
+// Request: worst-case gap before the 64 KB-aligned LUT + LUT + all stages
+// that do not fit in the gap (see step_fast_kernel).
+constexpr int kSmem = 65536 + kLutBytes + kWarps * kWarpStage - (65536 / kWarpStage - 1) * kWarpStage;
 
 template <int B, int E, typename F>
 __device__ __forceinline__ void static_for(F&& f) {
@@ -108,15 +110,26 @@ struct Raw {
   uint32_t e;  // lane 0: word left of the band; last lane: word right of it
 };
 
+// A source row as the motion needs it: its 16 bytes and the same bytes
+// shifted by one column either way (computed once per row and reused by the
+// three destination rows that read it).
 struct Row {
   uint32_t w[4];
-  uint32_t L;  // word whose top byte is column x0-1
-  uint32_t R;  // word whose low byte is column x0+16
+  uint32_t sl[4];  // column x-1 at every byte
+  uint32_t sr[4];  // column x+1 at every byte
 };
 
-struct Konst {  // run-time copies of StepArgs::k16 / k256 / k2p24
-  uint32_t k16, k256, k2p24;
+struct Konst {  // run-time copies of StepArgs::k1 / k16 / k256 / k2p24
+  uint32_t k1, k16, k256, k2p24;
 };
+
+// key + y as one IMAD.WIDE (FMA pipe) instead of a carry chain on the ALU
+// pipe: `one` is a run-time 1.
+__device__ __forceinline__ uint64_t add_wide(uint64_t key, uint32_t y, uint32_t one) {
+  uint64_t z;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(z) : "r"(y), "r"(one), "l"(key));
+  return z;
+}
 
 struct Lane {
   int lane, last;
@@ -137,17 +150,20 @@ __device__ __forceinline__ Row finish(const Raw& r, const Lane& ln) {
   o.w[3] = r.v.w;
   const uint32_t up = __shfl_up_sync(kFull, r.v.w, 1);
   const uint32_t dn = __shfl_down_sync(kFull, r.v.x, 1);
-  o.L = ln.lane == 0 ? r.e : up;
-  o.R = ln.lane == ln.last ? r.e : dn;
+  const uint32_t L = ln.lane == 0 ? r.e : up;         // top byte = column x0-1
+  const uint32_t R = ln.lane == ln.last ? r.e : dn;   // low byte = column x0+16
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    o.sl[j] = __byte_perm(j == 0 ? L : o.w[j - 1], o.w[j], 0x6543);
+    o.sr[j] = __byte_perm(o.w[j], j == 3 ? R : o.w[j + 1], 0x4321);
+  }
   return o;
 }
 
 // Column x-1 / x+1 at every byte of word j.
-__device__ __forceinline__ uint32_t shl1(const Row& r, int j) {
-  return __byte_perm(j == 0 ? r.L : r.w[j - 1], r.w[j], 0x6543);
-}
+__device__ __forceinline__ uint32_t shl1(const Row& r, int j) { return r.sl[j]; }
 __device__ __forceinline__ uint32_t shr1(const Row& r, int j) {
-  return __byte_perm(r.w[j], j == 3 ? r.R : r.w[j + 1], 0x4321);
+  return r.sr[j];
 }
 // (a & m) | (b & ~m) as one LOP3 (the compiler otherwise splits the chain
 // into AND + OR-AND pairs).
@@ -179,11 +195,13 @@ __device__ __forceinline__ uint32_t row_update(const Row& P, const Row& C, const
     m = mux<0x08080808u>(p3, m);
     m = mux<0x10101010u>(p4, m);
     m = mux<0x20202020u>(shr1(C, j), m);
-    // [laneoff.b0 (= lane*4), m.bk, 0, 0] -> state * 256 + lane * 4
-    const uint32_t v0 = lds32(lut + __byte_perm(laneoff, m, 0x1140));
-    const uint32_t v1 = lds32(lut + __byte_perm(laneoff, m, 0x1150));
-    const uint32_t v2 = lds32(lut + __byte_perm(laneoff, m, 0x1160));
-    const uint32_t v3 = lds32(lut + __byte_perm(laneoff, m, 0x1170));
+    // laneoff = LUT base (64 KB aligned) | lane * 4: [laneoff.b0, m.bk,
+    // laneoff.b2, laneoff.b3] is the full address of the lane's entry.
+    (void)lut;
+    const uint32_t v0 = lds32(__byte_perm(laneoff, m, 0x3240));
+    const uint32_t v1 = lds32(__byte_perm(laneoff, m, 0x3250));
+    const uint32_t v2 = lds32(__byte_perm(laneoff, m, 0x3260));
+    const uint32_t v3 = lds32(__byte_perm(laneoff, m, 0x3270));
     // Entries are out | xor << 16 with both < 256, so v0 + 256 v1 packs
     // [out_0, out_1, xor_0, xor_1] without carries (IMAD on the FMA pipe).
     const uint32_t A = v1 * K.k256 + v0;
@@ -191,16 +209,11 @@ __device__ __forceinline__ uint32_t row_update(const Row& P, const Row& C, const
     out0[j] = __byte_perm(A, B, 0x5410);
     dep[j] = __byte_perm(A, B, 0x7632);
   }
-  // 16-bit dep mask, bit 4j + b <-> byte b of word j: one multiply gathers
-  // the four flag bits (bit 7 of each byte) into bits 28..31, a high
-  // multiply extracts that nibble, a multiply-add places it.
-  uint32_t f = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t nib = __umulhi((dep[j] & 0x80808080u) * 0x00204081u, K.k16);
-    f = nib * (1u << (4 * j)) + f;
-  }
-  return f;
+  // Dep mask: bit 8b + 7 - j <-> byte b of word j (the flag bits shifted
+  // into the high nibble of each byte; a second row goes to the low nibbles).
+  const uint32_t FK = 0x80808080u;
+  return (dep[0] & FK) | ((dep[1] >> 1) & (FK >> 1)) | ((dep[2] >> 2) & (FK >> 2)) |
+         ((dep[3] >> 3) & (FK >> 3));
 }
 
 // One dep site handed to a walk callback.
@@ -219,8 +232,10 @@ __device__ __forceinline__ uint32_t top_bit(uint32_t m) {
 }
 
 // Load-balanced walk over the dep sites of a batch. Each lane holds two
-// masks, M01 (rows 0, 1) and M23 (rows 2, 3): bit 16*r' + c <-> row 2k+r',
-// column c of the lane's 16. The sites are numbered lane-major; every lane
+// masks, M01 (rows 0, 1) and M23 (rows 2, 3): bit 8b + 7 - (4r' + j) <->
+// row 2k+r', byte b of word j of the lane's 16 sites (the first row of a
+// pair in the high nibbles of the bytes, the second in the low nibbles).
+// The sites are numbered lane-major; every lane
 // takes an equal contiguous slice of that list (prefix sum + binary search
 // over lanes) and calls fn(site) for each.
 template <typename Fn>
@@ -262,7 +277,7 @@ __device__ __forceinline__ void warp_walk(uint32_t M01, uint32_t M23, uint32_t s
     uint32_t kbase = keys + (off >> 3) * 256u;
     uint32_t wbase = stage + (off >> 3) * 16u + (off & 4u) * 256u;
     uint32_t rbase = (off >> 1) & 2u;
-    for (int it = s; it < e; ++it) {
+    auto next = [&]() {
       while (mask == 0u) {
         off += 4u;
         mask = lds32(smask + off);
@@ -270,15 +285,24 @@ __device__ __forceinline__ void warp_walk(uint32_t M01, uint32_t M23, uint32_t s
         wbase = stage + (off >> 3) * 16u + (off & 4u) * 256u;
         rbase = (off >> 1) & 2u;
       }
-      const uint32_t p = top_bit(mask);
+      const uint32_t p = top_bit(mask);  // p = 8b + 7 - k, k = 4 * r1 + j
       mask ^= 1u << p;
-      const uint32_t r1 = p >> 4;  // second row of the pair
+      const uint32_t np = ~p;
+      const uint32_t j = np & 3u;         // word in the lane's 16 bytes
+      const uint32_t r1 = (np >> 2) & 1u;  // second row of the pair
       Site t;
       t.row = rbase + r1;
-      t.sh = (p & 3u) * 8u;
-      t.key = kbase + (p & 15u) * 8u;
-      t.word = wbase + r1 * 512u + (p & 12u);
-      fn(t);
+      t.sh = p & 0x18u;                    // 8 * byte
+      t.key = kbase + j * 32u + t.sh;      // column 4j + b, 8 bytes per key
+      t.word = wbase + r1 * 512u + j * 4u;
+      return t;
+    };
+    // Two sites per iteration: two independent RNG chains in flight per lane.
+    for (int it = s; it < e; it += 2) {
+      const Site t0 = next();
+      const bool has1 = it + 1 < e;
+      const Site t1 = has1 ? next() : t0;
+      fn(t0, t1, has1);
     }
   }
   __syncwarp();
@@ -292,8 +316,8 @@ __device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint3
   const size_t pitch = a.pitch;
   const uint32_t smask = stage + kStageMask;
   const uint32_t my = stage + ln.lane * 16;  // this lane's 16 bytes of a staged row
-  const uint32_t laneoff = ln.lane * 4u;
-  const Konst K{a.k16, a.k256, a.k2p24};
+  const uint32_t laneoff = lut | (ln.lane * 4u);  // lut is 64 KB aligned
+  const Konst K{a.k1, a.k16, a.k256, a.k2p24};
   uint32_t F[kBatch];
   static_for<0, kBatch>([&](auto ic) {
     constexpr int i = decltype(ic)::value;
@@ -308,16 +332,21 @@ __device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint3
       sts128(my + kStageDep + i * 512, d[0], d[1], d[2], d[3]);
     }
   });
-  uint32_t M01 = F[1] * 65536u + F[0], M23 = F[3] * 65536u + F[2];
+  uint32_t M01 = F[0] | (F[1] >> 4), M23 = F[2] | (F[3] >> 4);
   if (!ln.active) M01 = M23 = 0u;
   __syncwarp();
   const uint64_t ybase = static_cast<uint64_t>(a.row0 + rb);
+  const uint32_t y32 = static_cast<uint32_t>(a.row0 + rb);  // global rows < 2^31
   // Chirality: sites whose two outcomes differ (rng.hpp:25-33 keyed by the
   // 1-based storage column and global row, step.cpp:73-76).
-  warp_walk(M01, M23, smask, stage, keys, ln.lane, [&](const Site& t) {
-    const uint32_t chir = fin64_bit0(lds64(t.key) + ybase + t.row);
-    const uint32_t d = lds32(t.word + kStageDep) & (0x7Fu << t.sh);
-    atoms_xor(t.word, chir ? d : 0u);
+  warp_walk(M01, M23, smask, stage, keys, ln.lane,
+            [&](const Site& t0, const Site& t1, bool has1) {
+    const uint32_t c0 = fin64_bit0(add_wide(lds64(t0.key), y32 + t0.row, K.k1));
+    const uint32_t c1 = fin64_bit0(add_wide(lds64(t1.key), y32 + t1.row, K.k1)) & (has1 ? 1u : 0u);
+    const uint32_t d0 = lds32(t0.word + kStageDep) & (0x7Fu << t0.sh);
+    const uint32_t d1 = lds32(t1.word + kStageDep) & (0x7Fu << t1.sh);
+    atoms_xor(t0.word, d0 * c0);  // select by multiply (FMA pipe)
+    atoms_xor(t1.word, d1 * c1);
   });
   if (FORCE) {
     // Forcing on the post-collision state (step.cpp:79-88): fluid, W set, E clear.
@@ -331,18 +360,19 @@ __device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint3
         uint32_t g = 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          g = __umulhi((((w[j] >> 5) & ~(w[j] >> 2) & ~(w[j] >> 7)) & 0x01010101u) * 0x10204080u,
-                       K.k16) * (1u << (4 * j)) + g;
+          g |= (((w[j] >> 5) & ~(w[j] >> 2) & ~(w[j] >> 7)) & 0x01010101u) << (7 - j);
         G[i] = g;
       }
     });
-    uint32_t G01 = G[1] * 65536u + G[0], G23 = G[3] * 65536u + G[2];
+    uint32_t G01 = G[0] | (G[1] >> 4), G23 = G[2] | (G[3] >> 4);
     if (!ln.active) G01 = G23 = 0u;
-    warp_walk(G01, G23, smask, stage, keys + 128u * 256u, ln.lane, [&](const Site& t) {
-      if ((fin64(lds64(t.key) + ybase + t.row) >> 32) < a.thr) {
-        atoms_xor(t.word, 0x24u << t.sh);
-        ++swaps;
-      }
+    warp_walk(G01, G23, smask, stage, keys + 128u * 256u, ln.lane,
+              [&](const Site& t0, const Site& t1, bool has1) {
+      const bool f0 = (fin64(lds64(t0.key) + ybase + t0.row) >> 32) < a.thr;
+      const bool f1 = has1 && (fin64(lds64(t1.key) + ybase + t1.row) >> 32) < a.thr;
+      atoms_xor(t0.word, f0 ? 0x24u << t0.sh : 0u);
+      atoms_xor(t1.word, f1 ? 0x24u << t1.sh : 0u);
+      swaps += static_cast<unsigned>(f0) + static_cast<unsigned>(f1);
     });
   }
   static_for<0, kBatch>([&](auto ic) {
@@ -382,16 +412,24 @@ template <bool FORCE>
 __global__ void __launch_bounds__(kThreads, 1) step_fast_kernel(StepArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
+  // The LUT sits on a 64 KB boundary of the shared window, so one PRMT builds
+  // the complete LDS address (base bytes 2-3 | state << 8 | lane * 4) with no
+  // add. Warp stages fill the space before and after it.
+  const uint32_t lut_abs = (sbase + 0xFFFFu) & ~0xFFFFu;
+  const uint32_t kpre = (lut_abs - sbase) / kWarpStage;
   const int warp = threadIdx.x >> 5;
   const int band_group = blockIdx.x % a.nbands_groups;
   const int seg_group = blockIdx.x / a.nbands_groups;
   const int cta_x0 = band_group * kBandsPerCta * 512;
+  if (threadIdx.x == 0 &&
+      lut_abs + kLutBytes + (kWarps - umin(kpre, kWarps)) * kWarpStage > sbase + kSmem)
+    __trap();  // shared-memory map does not fit the request
   // LUT: lane-private words (e*256 + 4l) = out(ch0) | flagged XOR(ch0, ch1) << 16.
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     const int e = i >> 5, l = i & 31;
     const uint32_t o0 = a.table[e], o1 = a.table[256 + e];
     const uint32_t x = o0 ^ o1;
-    sts32(sbase + e * 256 + l * 4, o0 | ((x | (x ? 0x80u : 0u)) << 16));
+    sts32(lut_abs + e * 256 + l * 4, o0 | ((x | (x ? 0x80u : 0u)) << 16));
   }
   // Column keys of this CTA's 2048 columns into the LUT rows' second halves:
   // column c at row c >> 4, +128 + (c & 15) * 8 (a lane's 16 keys share a
@@ -399,8 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1) step_fast_kernel(StepArgs a) {
   for (int c = threadIdx.x; c < kBandsPerCta * 512; c += blockDim.x) {
     const int x = cta_x0 + c;
     if (x < a.W) {
-      sts64(sbase + (c >> 4) * 256 + 128 + (c & 15) * 8, a.zc[x]);
-      if (FORCE) sts64(sbase + (128 + (c >> 4)) * 256 + 128 + (c & 15) * 8, a.zf[x]);
+      sts64(lut_abs + (c >> 4) * 256 + 128 + (c & 15) * 8, a.zc[x]);
+      if (FORCE) sts64(lut_abs + (128 + (c >> 4)) * 256 + 128 + (c & 15) * 8, a.zf[x]);
     }
   }
   __syncthreads();
@@ -429,9 +467,11 @@ __global__ void __launch_bounds__(kThreads, 1) step_fast_kernel(StepArgs a) {
   ln.last = min(31, (a.W - band_x) / 16 - 1);
   ln.eoff = ln.lane == 0 ? (x0 == 0 ? a.W - 4 : x0 - 4)
                          : (ln.lane == ln.last ? (x0 + 16 == a.W ? 0 : x0 + 16) : ln.x0);
-  const uint32_t lut = sbase;
-  const uint32_t keys = sbase + bic * 32 * 256 + 128;  // a band's 512 keys: 32 LUT rows
-  const uint32_t stage = sbase + kLutBytes + warp * kWarpStage;
+  const uint32_t lut = lut_abs;
+  const uint32_t keys = lut_abs + bic * 32 * 256 + 128;  // a band's 512 keys: 32 LUT rows
+  const uint32_t stage = static_cast<uint32_t>(warp) < kpre
+                             ? sbase + warp * kWarpStage
+                             : lut_abs + kLutBytes + (warp - kpre) * kWarpStage;
   unsigned swaps = 0;
   if ((a.row0 + r_begin) & 1)
     run_segment<1, FORCE>(a, lut, keys, stage, ln, r_begin, r_end, swaps);
@@ -456,6 +496,7 @@ int launch_step_fast(const StepArgs& a0, int num_sms, cudaStream_t st) {
     attr_set = true;
   }
   const int rows = a.row_hi - a.row_lo;
+  a.k1 = 1u;
   a.k16 = 16u;
   a.k256 = 256u;
   a.k2p24 = 1u << 24;
