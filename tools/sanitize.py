@@ -1,0 +1,19 @@
+"""Small fast-path + generic-path runs for compute-sanitizer (memcheck,
+racecheck, initcheck): python tools/sanitize.py"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1208_2428_b200 as P  # noqa: E402
+
+for W, H, fp in ((1024, 64, 0.2), (528, 40, 0.0), (100, 23, 0.5)):
+    e = P.Engine(W, H)
+    e.set_table(P.build_table("fhp3"))
+    e.init(3, 0.3)
+    e.advance(3, fp, 0, 5)
+    e.observables()
+    e.cells(4)
+    e.rows()
+    e.download()
+    e.close()
+print("sanitize run ok")
