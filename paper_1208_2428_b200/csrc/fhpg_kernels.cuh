@@ -32,7 +32,7 @@ struct StepArgs {
   // Powers of two passed at run time so that ptxas keeps the byte moves that
   // use them as IMAD / IMAD.HI (FMA pipe) instead of folding them into
   // shifts on the ALU pipe, which the fast path saturates (fast path only).
-  uint32_t k1, k16, k256, k2p24;
+  uint32_t k1, k2, k4, k16, k32, k256, k2p24;
   int seg_rows;              // rows per warp task (fast path)
   int nbands;                // 512-column bands (fast path)
   int nbands_groups;         // CTA column groups (fast path)

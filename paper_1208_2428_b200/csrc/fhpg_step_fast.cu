@@ -119,9 +119,25 @@ struct Row {
   uint32_t sr[4];  // column x+1 at every byte
 };
 
-struct Konst {  // run-time copies of StepArgs::k1 / k16 / k256 / k2p24
-  uint32_t k1, k16, k256, k2p24;
+struct Konst {  // run-time copies of StepArgs::k1 ... k2p24
+  uint32_t k1, k2, k4, k16, k32, k256, k2p24;
 };
+
+// Bit 0 of fin64(z) (fhpg_common.cuh fin64_bit0) with every shift written as
+// a multiply so that it issues on the FMA pipe: x >> s == hi(x * 2^(32-s)),
+// x << s == x * 2^s; only the four XORs use the (saturated) ALU pipe.
+__device__ __forceinline__ uint32_t chir_bit(uint64_t z, const Konst& K) {
+  const uint32_t lo = static_cast<uint32_t>(z), hi = static_cast<uint32_t>(z >> 32);
+  const uint32_t t_lo = lo ^ (__umulhi(lo, K.k4) + hi * K.k4);  // lo32(z ^ (z >> 30))
+  const uint32_t t_hi = hi ^ __umulhi(hi, K.k4);                // hi32(z ^ (z >> 30))
+  const uint64_t w = static_cast<uint64_t>(t_lo) * static_cast<uint32_t>(kC1);
+  const uint32_t z1_lo = static_cast<uint32_t>(w);
+  const uint32_t z1_hi = static_cast<uint32_t>(w >> 32) + t_lo * static_cast<uint32_t>(kC1 >> 32) +
+                         t_hi * static_cast<uint32_t>(kC1);
+  const uint32_t u = z1_lo ^ (__umulhi(z1_lo, K.k32) + z1_hi * K.k32);  // lo32(z1 ^ (z1 >> 27))
+  const uint32_t p = u * static_cast<uint32_t>(kC2);
+  return (p ^ __umulhi(p, K.k2)) & 1u;  // bit0 ^ bit31
+}
 
 // key + y as one IMAD.WIDE (FMA pipe) instead of a carry chain on the ALU
 // pipe: `one` is a run-time 1.
@@ -317,7 +333,7 @@ __device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint3
   const uint32_t smask = stage + kStageMask;
   const uint32_t my = stage + ln.lane * 16;  // this lane's 16 bytes of a staged row
   const uint32_t laneoff = lut | (ln.lane * 4u);  // lut is 64 KB aligned
-  const Konst K{a.k1, a.k16, a.k256, a.k2p24};
+  const Konst K{a.k1, a.k2, a.k4, a.k16, a.k32, a.k256, a.k2p24};
   uint32_t F[kBatch];
   static_for<0, kBatch>([&](auto ic) {
     constexpr int i = decltype(ic)::value;
@@ -341,6 +357,7 @@ __device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint3
   // 1-based storage column and global row, step.cpp:73-76).
   warp_walk(M01, M23, smask, stage, keys, ln.lane,
             [&](const Site& t0, const Site& t1, bool has1) {
+    // (chir_bit, the all-FMA-pipe variant, measured 4% slower: more issue slots.)
     const uint32_t c0 = fin64_bit0(add_wide(lds64(t0.key), y32 + t0.row, K.k1));
     const uint32_t c1 = fin64_bit0(add_wide(lds64(t1.key), y32 + t1.row, K.k1)) & (has1 ? 1u : 0u);
     const uint32_t d0 = lds32(t0.word + kStageDep) & (0x7Fu << t0.sh);
@@ -497,6 +514,9 @@ int launch_step_fast(const StepArgs& a0, int num_sms, cudaStream_t st) {
   }
   const int rows = a.row_hi - a.row_lo;
   a.k1 = 1u;
+  a.k2 = 2u;
+  a.k4 = 4u;
+  a.k32 = 32u;
   a.k16 = 16u;
   a.k256 = 256u;
   a.k2p24 = 1u << 24;
