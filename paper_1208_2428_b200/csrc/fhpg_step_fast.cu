@@ -251,12 +251,57 @@ __device__ __forceinline__ uint32_t top_bit(uint32_t m) {
 // masks, M01 (rows 0, 1) and M23 (rows 2, 3): bit 8b + 7 - (4r' + j) <->
 // row 2k+r', byte b of word j of the lane's 16 sites (the first row of a
 // pair in the high nibbles of the bytes, the second in the low nibbles).
-// The sites are numbered lane-major; every lane
-// takes an equal contiguous slice of that list (prefix sum + binary search
-// over lanes) and calls fn(site) for each.
+// Phase 1: every lane takes floor(T/32) of its own sites (T = the warp's
+// total), a uniform trip count with no owner lookup. Phase 2: the sites left
+// over on busier lanes are numbered lane-major and every lane takes an equal
+// contiguous slice of that list (prefix sum + binary search over lanes).
+// fn(site0, valid0, site1, valid1) handles two sites per call.
+template <typename Fn>
+__device__ __forceinline__ void balanced_walk(uint32_t M01, uint32_t M23, uint32_t smask,
+                                              uint32_t stage, uint32_t keys, int lane, Fn&& fn);
+
 template <typename Fn>
 __device__ __forceinline__ void warp_walk(uint32_t M01, uint32_t M23, uint32_t smask,
                                           uint32_t stage, uint32_t keys, int lane, Fn&& fn) {
+  // Phase 1 measured slower (v11: 1207 vs 1267 GSUPS, same instruction
+  // count per site): the per-site overhead is the same whether the site is
+  // the lane's own or another lane's. Keep the single balanced phase.
+  constexpr bool kOwnPhase = false;
+  const int T = kOwnPhase ? static_cast<int>(__reduce_add_sync(kFull, __popc(M01) + __popc(M23))) : 0;
+  const int M = T >> 5;
+  const uint32_t kown = keys + static_cast<uint32_t>(lane) * 256u;
+  const uint32_t wown = stage + static_cast<uint32_t>(lane) * 16u;
+  auto own_next = [&](bool& valid) {
+    const bool useA = M01 != 0u;
+    const uint32_t m = useA ? M01 : M23;
+    valid = m != 0u;
+    const uint32_t p = top_bit(m);  // p = 8b + 7 - (4 r1 + j); 0xFFFFFFFF if m == 0
+    const uint32_t bit = valid ? (1u << p) : 0u;
+    if (useA) M01 ^= bit;
+    else M23 ^= bit;
+    const uint32_t np = ~p;
+    const uint32_t j = np & 3u;
+    const uint32_t r1 = (np >> 2) & 1u;
+    const uint32_t pr = useA ? 0u : 1u;
+    Site t;
+    t.row = pr * 2u + r1;
+    t.sh = p & 0x18u;
+    t.key = kown + j * 32u + t.sh;
+    t.word = wown + pr * 1024u + r1 * 512u + j * 4u;
+    return t;
+  };
+  for (int it = 0; it < M; it += 2) {  // M is warp-uniform
+    bool v0, v1 = false;
+    const Site t0 = own_next(v0);
+    const Site t1 = it + 1 < M ? own_next(v1) : t0;
+    fn(t0, v0, t1, v1);
+  }
+  balanced_walk(M01, M23, smask, stage, keys, lane, fn);
+}
+
+template <typename Fn>
+__device__ __forceinline__ void balanced_walk(uint32_t M01, uint32_t M23, uint32_t smask,
+                                              uint32_t stage, uint32_t keys, int lane, Fn&& fn) {
   const int cnt = __popc(M01) + __popc(M23);
   int incl = cnt;
 #pragma unroll
@@ -318,7 +363,7 @@ __device__ __forceinline__ void warp_walk(uint32_t M01, uint32_t M23, uint32_t s
       const Site t0 = next();
       const bool has1 = it + 1 < e;
       const Site t1 = has1 ? next() : t0;
-      fn(t0, t1, has1);
+      fn(t0, true, t1, has1);
     }
   }
   __syncwarp();
@@ -356,9 +401,9 @@ __device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint3
   // Chirality: sites whose two outcomes differ (rng.hpp:25-33 keyed by the
   // 1-based storage column and global row, step.cpp:73-76).
   warp_walk(M01, M23, smask, stage, keys, ln.lane,
-            [&](const Site& t0, const Site& t1, bool has1) {
+            [&](const Site& t0, bool has0, const Site& t1, bool has1) {
     // (chir_bit, the all-FMA-pipe variant, measured 4% slower: more issue slots.)
-    const uint32_t c0 = fin64_bit0(add_wide(lds64(t0.key), y32 + t0.row, K.k1));
+    const uint32_t c0 = fin64_bit0(add_wide(lds64(t0.key), y32 + t0.row, K.k1)) & (has0 ? 1u : 0u);
     const uint32_t c1 = fin64_bit0(add_wide(lds64(t1.key), y32 + t1.row, K.k1)) & (has1 ? 1u : 0u);
     const uint32_t d0 = lds32(t0.word + kStageDep) & (0x7Fu << t0.sh);
     const uint32_t d1 = lds32(t1.word + kStageDep) & (0x7Fu << t1.sh);
@@ -384,8 +429,8 @@ __device__ __forceinline__ void run_batch(const StepArgs& a, uint32_t lut, uint3
     uint32_t G01 = G[0] | (G[1] >> 4), G23 = G[2] | (G[3] >> 4);
     if (!ln.active) G01 = G23 = 0u;
     warp_walk(G01, G23, smask, stage, keys + 128u * 256u, ln.lane,
-              [&](const Site& t0, const Site& t1, bool has1) {
-      const bool f0 = (fin64(lds64(t0.key) + ybase + t0.row) >> 32) < a.thr;
+              [&](const Site& t0, bool has0, const Site& t1, bool has1) {
+      const bool f0 = has0 && (fin64(lds64(t0.key) + ybase + t0.row) >> 32) < a.thr;
       const bool f1 = has1 && (fin64(lds64(t1.key) + ybase + t1.row) >> 32) < a.thr;
       atoms_xor(t0.word, f0 ? 0x24u << t0.sh : 0u);
       atoms_xor(t1.word, f1 ? 0x24u << t1.sh : 0u);
