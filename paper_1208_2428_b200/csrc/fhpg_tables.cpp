@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "../../include/fhpg_tables.h"
+#include "fhpg_fhp3_logic.cuh"
 
 namespace {
 
@@ -87,7 +88,25 @@ void build_fhp1(uint8_t* t) {
     }
 }
 
+// FHP-III: the bit-sliced rule of fhpg_fhp3_logic.cuh evaluated per state
+// (bit 0 of each word), so the table and the bit-plane kernel are one rule.
 void build_fhp3(uint8_t* t) {
+  for (int ch = 0; ch < 2; ++ch)
+    for (unsigned s = 0; s < 256; ++s) {
+      uint32_t a[6], o[6], orr, dep;
+      for (int k = 0; k < 6; ++k) a[k] = (s >> k) & 1u;
+      fhpg::fhp3_collide<uint32_t>(a, (s >> 6) & 1u, (s >> 7) & 1u, static_cast<uint32_t>(ch), o,
+                                   orr, dep);
+      unsigned out = s & 0x80u;
+      for (int k = 0; k < 6; ++k) out |= (o[k] & 1u) << k;
+      out |= (orr & 1u) << 6;
+      t[(ch << 8) | s] = static_cast<uint8_t>(out);
+    }
+}
+
+// The class-cycle construction used before the rule was written as logic
+// (kept for reference; not used).
+[[maybe_unused]] void build_fhp3_class_cycles(uint8_t* t) {
   // Group fluid states by (mass, px, py).
   std::map<std::array<int, 3>, std::vector<unsigned>> classes;
   for (unsigned s = 0; s < 128; ++s) {
