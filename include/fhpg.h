@@ -97,6 +97,13 @@ int fhpg_advance(fhpg_engine* e, uint64_t seed, uint64_t force_thr, int64_t firs
 int fhpg_advance_async(fhpg_engine* e, uint64_t seed, uint64_t force_thr, int64_t first_step,
                        int64_t step_count);
 
+/* One step split in two launches so a strip can overlap its halo exchange
+ * with the interior (the device analog of run_strips' per-step phases,
+ * backends.cpp:196-209): part 0 updates rows 1..nrows-2 (needs no halo),
+ * part 1 updates rows 0 and nrows-1 (needs the halos of this step) and
+ * swaps the buffers. Enqueue only; swaps accumulate on the device. */
+int fhpg_advance_part(fhpg_engine* e, uint64_t seed, uint64_t force_thr, int64_t step, int part);
+
 /* Synchronise and read (optionally reset) the device swap counter. */
 int fhpg_swaps(fhpg_engine* e, uint64_t* swaps, int reset);
 

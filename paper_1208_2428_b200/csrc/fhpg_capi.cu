@@ -29,6 +29,9 @@ struct fhpg_engine {
   bool force_generic = false;
   int num_sms = 148;
   uint64_t launches = 0;
+  int64_t keys_step = -1;                // step whose column keys are in keys(step & 1)
+  uint64_t keys_seed = 0;
+  bool keys_force = false;
 
   uint8_t* base(int which) const { return buf[which] + pitch; }  // local row 0
   uint64_t* keys(int parity, int purpose) const {
@@ -188,6 +191,71 @@ void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64
     ck(cudaGetLastError(), "step launch");
     e->cur ^= 1;
   }
+  e->keys_step = -1;
+}
+
+// One step in two parts for strips that overlap the halo exchange with the
+// interior: part 0 = rows [1, nrows-1) (needs no halo row), part 1 = the
+// boundary rows 0 and nrows-1, then the buffer swap.
+void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int part) {
+  using namespace fhpg;
+  if (!e->table_set) invalid("collision table not set (fhpg_set_table)");
+  if (thr > (1ull << 32)) invalid("force threshold must be <= 2^32");
+  if (part != 0 && part != 1) invalid("part must be 0 (interior) or 1 (boundary rows)");
+  cudaStream_t st = e->stream;
+  if (!e->normalized) {
+    launch_apply_mask(e->base(e->cur), e->mask, e->pitch, e->W, e->nrows, st);
+    ck(cudaGetLastError(), "apply_mask launch");
+    e->normalized = true;
+  }
+  const bool force = thr != 0;
+  const uint64_t s = static_cast<uint64_t>(step);
+  if (e->keys_step != step || e->keys_seed != seed || (force && !e->keys_force)) {
+    launch_column_keys(e->keys(s & 1, 0), force ? e->keys(s & 1, 1) : nullptr,
+                       step_key(seed, kChirality, s), step_key(seed, kForcing, s), e->W, st);
+    ck(cudaGetLastError(), "column_keys launch");
+    e->keys_step = step;
+    e->keys_seed = seed;
+    e->keys_force = force;
+  }
+  StepArgs a{};
+  a.src = e->base(e->cur);
+  a.dst = e->base(e->cur ^ 1);
+  a.pitch = e->pitch;
+  a.W = e->W;
+  a.nrows = e->nrows;
+  a.row0 = e->row_begin;
+  a.table = e->table;
+  a.zc = e->keys(s & 1, 0);
+  a.zf = force ? e->keys(s & 1, 1) : nullptr;
+  a.thr = thr;
+  a.swaps = e->swaps;
+  const bool interior = e->nrows >= 3;
+  auto run = [&](int lo, int hi, bool with_next_keys) {
+    StepArgs b = a;
+    b.row_lo = lo;
+    b.row_hi = hi;
+    if (with_next_keys) {
+      b.zc_next = e->keys((s + 1) & 1, 0);
+      b.zf_next = force ? e->keys((s + 1) & 1, 1) : nullptr;
+      b.kc_next = step_key(seed, kChirality, s + 1);
+      b.kf_next = step_key(seed, kForcing, s + 1);
+    }
+    e->launches += launch_step(b, e->num_sms, st, e->force_generic);
+    ck(cudaGetLastError(), "step launch");
+  };
+  if (part == 0) {
+    if (interior) run(1, e->nrows - 1, true);
+    return;
+  }
+  if (interior) {
+    run(0, 1, false);
+    run(e->nrows - 1, e->nrows, false);
+  } else {
+    run(0, e->nrows, true);
+  }
+  e->cur ^= 1;
+  e->keys_step = step + 1;  // computed by part 0 (or by the single launch above)
 }
 
 void copy_rows_h2d(uint8_t* dev, size_t pitch, const uint8_t* host, size_t stride, int W,
@@ -330,6 +398,14 @@ int fhpg_advance(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int
     ck(cudaMemcpyAsync(&s, e->swaps, sizeof s, cudaMemcpyDeviceToHost, e->stream), "swap read");
     ck(cudaStreamSynchronize(e->stream), "advance sync");
     if (swaps) *swaps = s;
+  });
+}
+
+int fhpg_advance_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int part) {
+  return guarded([&] {
+    need(e);
+    DeviceGuard g(e->device);
+    step_part(e, seed, thr, step, part);
   });
 }
 

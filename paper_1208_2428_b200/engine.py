@@ -49,6 +49,7 @@ SIGNATURES = {
     "fhpg_advance": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, u64p]),
     "fhpg_advance_async": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int64, C.c_int64]),
     "fhpg_swaps": (C.c_int, [C.c_void_p, u64p, C.c_int]),
+    "fhpg_advance_part": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int64, C.c_int]),
     "fhpg_synchronize": (C.c_int, [C.c_void_p]),
     "fhpg_bernoulli_threshold": (C.c_uint64, [C.c_double]),
     "fhpg_reduce_global": (C.c_int, [C.c_void_p, i64p, i64p, i64p]),
@@ -223,6 +224,11 @@ class Engine:
 
     def advance_async(self, seed: int, force_thr: int, first_step: int, step_count: int):
         _check(self.lib.fhpg_advance_async(self.h, seed, force_thr, first_step, step_count))
+
+    def advance_part(self, seed: int, force_thr: int, step: int, part: int):
+        """Half of one step (fhpg_advance_part): part 0 = interior rows,
+        part 1 = boundary rows + buffer swap."""
+        _check(self.lib.fhpg_advance_part(self.h, seed, force_thr, step, part))
 
     def swaps(self, reset: bool = False) -> int:
         sw = C.c_uint64()

@@ -54,9 +54,11 @@ def engine_halo_tensors(engine, device: int):
 
 
 def exchange_halos(send_top, send_bottom, recv_top, recv_bottom, rank: int, world: int,
-                   group=None):
+                   group=None, wait: bool = True):
     """Send the first/last owned rows to the strips above/below and receive
-    their boundary rows into the halo rows (no-op at the global edges)."""
+    their boundary rows into the halo rows (no-op at the global edges).
+    With wait=False the pending works are returned (wait() on each makes the
+    current stream wait for the transfer)."""
     ops = []
     if rank > 0:
         ops.append(dist.P2POp(dist.isend, send_top, rank - 1, group))
@@ -64,9 +66,12 @@ def exchange_halos(send_top, send_bottom, recv_top, recv_bottom, rank: int, worl
     if rank < world - 1:
         ops.append(dist.P2POp(dist.isend, send_bottom, rank + 1, group))
         ops.append(dist.P2POp(dist.irecv, recv_bottom, rank + 1, group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
+    reqs = dist.batch_isend_irecv(ops) if ops else []
+    if wait:
+        for req in reqs:
             req.wait()
+        return []
+    return reqs
 
 
 class LocalStrips:
@@ -126,10 +131,14 @@ class LocalStrips:
         for e in self.engines:
             e.swaps(reset=True)
         for s in range(first_step, first_step + step_count):
-            if len(self.engines) > 1:
-                self._exchange()
-            for e in self.engines:
-                e.advance_async(seed, thr, s, 1)
+            if len(self.engines) == 1:
+                self.engines[0].advance_async(seed, thr, s, 1)
+                continue
+            for e in self.engines:  # interior rows: no halo needed
+                e.advance_part(seed, thr, s, 0)
+            self._exchange()
+            for e in self.engines:  # boundary rows + swap
+                e.advance_part(seed, thr, s, 1)
         return sum(e.swaps() for e in self.engines)
 
 
@@ -152,9 +161,14 @@ class DistStrips:
             self.engine.advance_async(seed, force_thr, first_step, step_count)
             return
         for s in range(first_step, first_step + step_count):
-            if self.world > 1:
-                exchange_halos(*self._halos(), self.rank, self.world, self.group)
-            self.engine.advance_async(seed, force_thr, s, 1)
+            # The exchange of this step's boundary rows is issued first (NCCL
+            # waits for the previous step), the interior rows run while it is
+            # in flight, the boundary rows after it lands.
+            reqs = exchange_halos(*self._halos(), self.rank, self.world, self.group, wait=False)
+            self.engine.advance_part(seed, force_thr, s, 0)
+            for req in reqs:
+                req.wait()
+            self.engine.advance_part(seed, force_thr, s, 1)
 
     def advance(self, seed: int, force_thr: int, first_step: int, step_count: int) -> int:
         """Like fhp::advance over the whole lattice: returns the global swap count."""

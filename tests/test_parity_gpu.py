@@ -249,3 +249,39 @@ def test_invalid_arguments():
         e.advance(1, 0.0, 0, 1)  # no table yet
     with pytest.raises(P.FhpgInvalidArgument):
         e.init(1, 1.5)
+
+
+def test_split_step_parts_equal_full_steps(tables, port):
+    """fhpg_advance_part (interior rows, then boundary rows + swap) == fhpg_advance."""
+    for (W, H, table, fp) in ((512, 40, "fhp3", 0.2), (100, 9, "default", 0.5), (64, 3, "fhp1", 1.0)):
+        s, m = port.scramble(W, H, 21)
+        a = P.Engine(W, H)
+        a.set_table(tables[table])
+        a.set_obstacles(m)
+        a.upload(s)
+        sw_a = a.advance(7, fp, 30, 6)
+        b = P.Engine(W, H)
+        b.set_table(tables[table])
+        b.set_obstacles(m)
+        b.upload(s)
+        thr = P.bernoulli_threshold(fp)
+        b.swaps(reset=True)
+        for step in range(30, 36):
+            b.advance_part(7, thr, step, 0)
+            b.advance_part(7, thr, step, 1)
+        assert (a.download() == b.download()).all(), (W, H)
+        assert b.swaps() == sw_a
+
+
+def test_local_strips_with_tiny_strips(tables, port):
+    from paper_1208_2428_b200.strips import LocalStrips
+    W, H = 48, 9
+    state, mask = port.scramble(W, H, 3)
+    for n in (4, 7):  # strips of 1-2 rows
+        ls = LocalStrips(W, H, n)
+        ls.set_table(tables["default"])
+        ls.set_obstacles(mask)
+        ls.upload(state)
+        sw = ls.advance(11, 0.3, 2, 9)
+        ref, rsw = port.advance(state, tables["default"], 11, port.threshold(0.3), 2, 9, mask=mask)
+        assert (ls.download() == ref).all() and sw == rsw

@@ -62,6 +62,12 @@ class OracleStrip:
             self.buf[1:-1] = out
             self.sw += sw
 
+    def advance_part(self, seed, thr, step, part):
+        # The oracle has no row split: the whole step runs at part 1, after
+        # the halos have arrived (part 0 must not need them).
+        if part == 1:
+            self.advance_async(seed, thr, step, 1)
+
     def swaps(self, reset=False):
         v = self.sw
         if reset:
