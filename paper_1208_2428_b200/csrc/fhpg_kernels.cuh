@@ -36,6 +36,7 @@ struct StepArgs {
   int seg_rows;              // rows per warp task (fast path)
   int nbands;                // 512-column bands (fast path)
   int nbands_groups;         // CTA column groups (fast path)
+  int bpc, spc;              // bands x segments per CTA (fast path)
   int row_lo, row_hi;        // local row range to update, [row_lo, row_hi)
 };
 

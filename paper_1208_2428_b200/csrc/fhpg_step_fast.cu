@@ -11,7 +11,7 @@
 // band (16 sites per lane: one 128-bit load and one 128-bit store per lane and
 // row) and a segment of rows it streams top to bottom, keeping rows r-1, r,
 // r+1 in registers so every source row is read from HBM once. A CTA covers
-// kBandsPerCta adjacent bands x kSegsPerCta segments.
+// up to kBandsPerCta adjacent bands x kWarps / bands segments.
 //
 // Per row: motion = byte permutes (PRMT, the +-1 column shifts, neighbour
 // lane edge bytes via SHFL) and LOP3 bit-select merges; collision = one LDS
@@ -42,7 +42,6 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kThreads = 640;
 constexpr int kWarps = kThreads / 32;
 constexpr int kBandsPerCta = 4;
-constexpr int kSegsPerCta = kWarps / kBandsPerCta;
 constexpr int kBatch = 4;
 // Shared memory map (bytes). The LUT uses the first 128 B of every 256-B
 // entry row; the second halves hold the column keys of the CTA's 2048
@@ -70,6 +69,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ uint64_t lds64(uint32_t a) {
@@ -482,26 +486,44 @@ __global__ void __launch_bounds__(kThreads, 1) step_fast_kernel(StepArgs a) {
   const int warp = threadIdx.x >> 5;
   const int band_group = blockIdx.x % a.nbands_groups;
   const int seg_group = blockIdx.x / a.nbands_groups;
-  const int cta_x0 = band_group * kBandsPerCta * 512;
+  const int cta_x0 = band_group * a.bpc * 512;
   if (threadIdx.x == 0 &&
       lut_abs + kLutBytes + (kWarps - umin(kpre, kWarps)) * kWarpStage > sbase + kSmem)
     __trap();  // shared-memory map does not fit the request
+  // The prologue is latency-bound on small lattices: every global load is
+  // issued before the first dependent shared store.
+  // Column keys of this CTA's columns (up to 2048) into the LUT rows' second
+  // halves: column c at row c >> 4, +128 + (c & 15) * 8 (a lane's 16 keys
+  // share a row); forcing keys 128 rows further.
+  constexpr int kKeyIters = (kBandsPerCta * 512 + kThreads - 1) / kThreads;
+  uint64_t kc[kKeyIters], kf[kKeyIters];
+#pragma unroll
+  for (int j = 0; j < kKeyIters; ++j) {
+    const int c = threadIdx.x + j * kThreads;
+    const bool ok = c < a.bpc * 512 && cta_x0 + c < a.W;
+    kc[j] = ok ? a.zc[cta_x0 + c] : 0;
+    kf[j] = ok && FORCE ? a.zf[cta_x0 + c] : 0;
+  }
+  // The 512-byte table goes through shared memory once (warp 0's stage,
+  // free until the second barrier).
+  const uint32_t tab = kpre > 0 ? sbase : lut_abs + kLutBytes;
+  if (threadIdx.x < 128)
+    sts32(tab + threadIdx.x * 4, reinterpret_cast<const uint32_t*>(a.table)[threadIdx.x]);
+#pragma unroll
+  for (int j = 0; j < kKeyIters; ++j) {
+    const int c = threadIdx.x + j * kThreads;
+    if (c < a.bpc * 512 && cta_x0 + c < a.W) {
+      sts64(lut_abs + (c >> 4) * 256 + 128 + (c & 15) * 8, kc[j]);
+      if (FORCE) sts64(lut_abs + (128 + (c >> 4)) * 256 + 128 + (c & 15) * 8, kf[j]);
+    }
+  }
+  __syncthreads();
   // LUT: lane-private words (e*256 + 4l) = out(ch0) | flagged XOR(ch0, ch1) << 16.
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     const int e = i >> 5, l = i & 31;
-    const uint32_t o0 = a.table[e], o1 = a.table[256 + e];
+    const uint32_t o0 = lds8(tab + e), o1 = lds8(tab + 256 + e);
     const uint32_t x = o0 ^ o1;
     sts32(lut_abs + e * 256 + l * 4, o0 | ((x | (x ? 0x80u : 0u)) << 16));
-  }
-  // Column keys of this CTA's 2048 columns into the LUT rows' second halves:
-  // column c at row c >> 4, +128 + (c & 15) * 8 (a lane's 16 keys share a
-  // row); forcing keys 128 rows further.
-  for (int c = threadIdx.x; c < kBandsPerCta * 512; c += blockDim.x) {
-    const int x = cta_x0 + c;
-    if (x < a.W) {
-      sts64(lut_abs + (c >> 4) * 256 + 128 + (c & 15) * 8, a.zc[x]);
-      if (FORCE) sts64(lut_abs + (128 + (c >> 4)) * 256 + 128 + (c & 15) * 8, a.zf[x]);
-    }
   }
   __syncthreads();
   // Next step's column keys (read by the next launch only).
@@ -513,11 +535,11 @@ __global__ void __launch_bounds__(kThreads, 1) step_fast_kernel(StepArgs a) {
     }
   }
 
-  const int bic = warp % kBandsPerCta;
-  const int band = band_group * kBandsPerCta + bic;
-  const int seg = seg_group * kSegsPerCta + warp / kBandsPerCta;
+  const int bic = warp % a.bpc;
+  const int band = band_group * a.bpc + bic;
+  const int seg = seg_group * a.spc + warp / a.bpc;
   const int r_begin = a.row_lo + seg * a.seg_rows;
-  if (band >= a.nbands || r_begin >= a.row_hi) return;  // whole warp
+  if (warp >= a.bpc * a.spc || band >= a.nbands || r_begin >= a.row_hi) return;  // whole warp
   const int r_end = min(a.row_hi, r_begin + a.seg_rows);
 
   Lane ln;
@@ -566,15 +588,19 @@ int launch_step_fast(const StepArgs& a0, int num_sms, cudaStream_t st) {
   a.k256 = 256u;
   a.k2p24 = 1u << 24;
   a.nbands = (a.W + 511) / 512;
-  a.nbands_groups = (a.nbands + kBandsPerCta - 1) / kBandsPerCta;
-  // One wave: at most num_sms CTAs (one per SM), each kSegsPerCta segments deep.
+  // Narrow lattices put fewer bands and more row segments in a CTA so that
+  // all 20 warps stay busy.
+  a.bpc = a.nbands < kBandsPerCta ? a.nbands : kBandsPerCta;
+  a.spc = kWarps / a.bpc;
+  a.nbands_groups = (a.nbands + a.bpc - 1) / a.bpc;
+  // One wave: at most num_sms CTAs (one per SM), each a.spc segments deep.
   int seg_groups = num_sms / a.nbands_groups;
   if (seg_groups < 1) seg_groups = 1;
-  int seg = (rows + seg_groups * kSegsPerCta - 1) / (seg_groups * kSegsPerCta);
-  if (seg < 8) seg = 8;
+  int seg = (rows + seg_groups * a.spc - 1) / (seg_groups * a.spc);
+  if (seg < kBatch) seg = kBatch;
   a.seg_rows = seg;
   const int nseg = (rows + seg - 1) / seg;
-  seg_groups = (nseg + kSegsPerCta - 1) / kSegsPerCta;
+  seg_groups = (nseg + a.spc - 1) / a.spc;
   const int grid = a.nbands_groups * seg_groups;
   if (a.thr != 0) step_fast_kernel<true><<<grid, kThreads, kSmem, st>>>(a);
   else step_fast_kernel<false><<<grid, kThreads, kSmem, st>>>(a);

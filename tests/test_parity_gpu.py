@@ -105,6 +105,23 @@ def test_chunked_advance_equals_single_call(tables, port):
     assert (a.download() == b.download()).all() and swa == swb
 
 
+@pytest.mark.parametrize("W", [512, 1024, 1536, 2048, 2560, 3584])
+def test_fast_path_cta_shapes(W, tables, port):
+    # 1..4 bands per CTA (narrow lattices trade bands for row segments),
+    # partial last band group, segments down to one 4-row batch.
+    for H in (37, 301):
+        s, m = port.scramble(W, H, W + H)
+        ref, rsw = port.advance(s, tables["fhp3"], 11, port.threshold(0.1), 5, 6, mask=m)
+        e = P.Engine(W, H)
+        assert e.fast_path
+        e.set_table(tables["fhp3"])
+        e.set_obstacles(m)
+        e.upload(s)
+        sw = e.advance(11, 0.1, 5, 6)
+        assert (e.download() == ref).all(), (W, H)
+        assert sw == rsw
+
+
 @pytest.mark.parametrize("case", range(40))
 def test_fuzz_against_oracle(case, port, tables):
     rng = np.random.default_rng(1000 + case)
