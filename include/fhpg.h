@@ -113,6 +113,11 @@ int fhpg_synchronize(fhpg_engine* e);
 /* rng.hpp:37-42 threshold: p >= 1 ? 2^32 : (uint64_t)(p * 2^32). */
 uint64_t fhpg_bernoulli_threshold(double p);
 
+/* FNV-1a-64 over n host bytes: the reference's state_digest
+ * (lattice.cpp:122-132) of a downloaded lattice (rows x W bytes, bit 7
+ * included); also the checkpoint integrity digest. Host-side, no engine. */
+uint64_t fhpg_digest(const uint8_t* bytes, size_t n);
+
 /* Integer observables of the engine's rows (observables.cpp:27-47):
  * mass = sum popcount(s & 0x7F) over all nodes, momentum over fluid nodes. */
 int fhpg_reduce_global(fhpg_engine* e, int64_t* mass, int64_t* px, int64_t* py);

@@ -5,4 +5,4 @@ include/fhpg.h) and the C++ host layer (paper_1208_2428_b200/host). This
 package is the thin Python binding used by tests and bench.py.
 """
 from .engine import (Engine, FhpgError, FhpgInvalidArgument, bernoulli_threshold,  # noqa: F401
-                     build_table, load_library, validate_table)
+                     build_table, load_library, state_digest, validate_table)

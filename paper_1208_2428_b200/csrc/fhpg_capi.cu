@@ -272,6 +272,12 @@ const char* fhpg_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t fhpg_bernoulli_threshold(double p) { return fhpg::bernoulli_threshold(p); }
 
+uint64_t fhpg_digest(const uint8_t* bytes, size_t n) {
+  uint64_t h = 0xCBF29CE484222325ull;
+  for (size_t i = 0; i < n; ++i) h = (h ^ bytes[i]) * 0x100000001B3ull;
+  return h;
+}
+
 int fhpg_create(int width, int height, fhpg_engine** out) {
   return guarded([&] {
     int dev = 0;

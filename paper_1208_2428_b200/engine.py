@@ -52,6 +52,7 @@ SIGNATURES = {
     "fhpg_advance_part": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_int64, C.c_int]),
     "fhpg_synchronize": (C.c_int, [C.c_void_p]),
     "fhpg_bernoulli_threshold": (C.c_uint64, [C.c_double]),
+    "fhpg_digest": (C.c_uint64, [C.c_void_p, C.c_size_t]),
     "fhpg_reduce_global": (C.c_int, [C.c_void_p, i64p, i64p, i64p]),
     "fhpg_reduce_cells": (C.c_int, [C.c_void_p, C.c_int, i32p, i32p, i64p, i64p]),
     "fhpg_reduce_rows": (C.c_int, [C.c_void_p, i64p, i32p]),
@@ -107,6 +108,13 @@ def _check(rc):
 def bernoulli_threshold(p: float) -> int:
     """rng.hpp:37-42 threshold (computed by the library, same double expression)."""
     return int(load_library().fhpg_bernoulli_threshold(float(p)))
+
+
+def state_digest(state) -> int:
+    """FNV-1a-64 of a downloaded lattice (the reference's state_digest,
+    lattice.cpp:122-132), computed by the native library."""
+    a = np.ascontiguousarray(state, dtype=np.uint8)
+    return int(load_library().fhpg_digest(a.ctypes.data, a.nbytes))
 
 
 def build_table(variant: str = "default") -> np.ndarray:

@@ -2,6 +2,7 @@
 // fhp_b200), the B200 counterpart of the reference's proj/core/include/fhp.
 #pragma once
 #include "fhp_b200/bench.hpp"
+#include "fhp_b200/checkpoint.hpp"
 #include "fhp_b200/collision.hpp"
 #include "fhp_b200/config.hpp"
 #include "fhp_b200/engine.hpp"

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "fhp_b200/bench.hpp"
+#include "fhp_b200/checkpoint.hpp"
 #include "fhp_b200/collision.hpp"
 #include "fhp_b200/observables.hpp"
 #include "fhp_b200/step.hpp"
@@ -27,6 +28,7 @@ namespace {
                               "[--density d] [--force-p p] [--seed s] [--rules default|fhp1|fhp3] "
                               "[--table-file F] [--geometry-file F] [--clear-rest] [--device D] "
                               "[--dump-every K --out-prefix P] [--repeats R --warmup W]\n"
+                              "       [--checkpoint-file F [--checkpoint-every K]] [--resume F]\n"
                               "       fhp_b200 tablegen OUTPUT [--rules ...]\n"
                               "       fhp_b200 validate FILE\n"
                               "       fhp_b200 geometry OUTPUT --width W --height H --cylinder");
@@ -69,6 +71,9 @@ Args parse(int argc, char** argv) {
     else if (k == "--warmup") a.cfg.warmup_steps = std::stoi(val());
     else if (k == "--device") a.cfg.device = std::stoi(val());
     else if (k == "--clear-rest") a.cfg.clear_rest = true;
+    else if (k == "--checkpoint-file") a.cfg.checkpoint_file = val();
+    else if (k == "--checkpoint-every") a.cfg.checkpoint_every = std::stoi(val());
+    else if (k == "--resume") a.cfg.resume_file = val();
     else if (k == "--cylinder") a.cylinder = true;
     else if (k == "--backend") {
       if (val() != "cuda") usage("fhp_b200 provides --backend cuda only");
@@ -87,8 +92,20 @@ void dump_outputs(const SimConfig& cfg, int step, const Engine& e) {
   write_density_pgm_file(tag + "_density.pgm", field);
 }
 
-int cmd_run(const SimConfig& cfg) {
-  const auto result = run(cfg, table_for(cfg), {},
+int cmd_run(SimConfig cfg) {
+  CollisionTable table;
+  if (!cfg.resume_file.empty()) {
+    // --resume: size, seed, force-p and table come from the checkpoint.
+    const Checkpoint ck = read_checkpoint_file(cfg.resume_file);
+    cfg.width = ck.width;
+    cfg.height = ck.height;
+    cfg.seed = ck.seed;
+    cfg.force_p = ck.force_p;
+    table = ck.table;
+  } else {
+    table = table_for(cfg);
+  }
+  const auto result = run(cfg, table, {},
                           [&cfg](int step, const Engine& e) { dump_outputs(cfg, step, e); });
   const auto& last = result.series.back();
   std::cout << "steps " << cfg.steps << "  mass " << last.mass << "  momentum ("

@@ -100,3 +100,28 @@ def test_cli_bench(tmp_path):
     assert r.returncode == 0, r.stderr
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 2 and '"backend":"cuda"' in lines[0]
+
+
+@pytest.mark.gpu
+def test_cli_checkpoint_resume(tmp_path):
+    # f4: run 60 steps straight == run 25 (checkpoint every 10) + resume to 60.
+    common = ["--width", "48", "--height", "33", "--density", "0.35", "--force-p", "0.01",
+              "--seed", "5"]
+    r = run(CLI, "run", "--steps", "60", *common)
+    assert r.returncode == 0 and "digest 0xf088af706ca84065" in r.stdout, r.stderr
+    ck = tmp_path / "ck.bin"
+    a = run(CLI, "run", "--steps", "25", *common, "--checkpoint-file", str(ck),
+            "--checkpoint-every", "10")
+    assert a.returncode == 0, a.stderr
+    from paper_1208_2428_b200 import checkpoint as K
+    c = K.load(str(ck))
+    assert (c.width, c.height, c.next_step, c.seed, c.force_p) == (48, 33, 25, 5, 0.01)
+    b = run(CLI, "run", "--steps", "60", "--resume", str(ck))
+    assert b.returncode == 0, b.stderr
+    assert "digest 0xf088af706ca84065" in b.stdout and "forcing_swaps 180" in b.stdout
+    # mismatching resume requests are invalid_argument (exit 2); a corrupt file exit 3
+    assert run(CLI, "run", "--steps", "20", "--resume", str(ck)).returncode == 2
+    raw = bytearray(ck.read_bytes())
+    raw[-1] ^= 1
+    (tmp_path / "bad.bin").write_bytes(bytes(raw))
+    assert run(CLI, "run", "--steps", "60", "--resume", str(tmp_path / "bad.bin")).returncode == 3
