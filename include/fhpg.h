@@ -141,13 +141,20 @@ int fhpg_halo(fhpg_engine* e, void** send_top, void** send_bottom, void** recv_t
               void** recv_bottom, size_t* row_bytes);
 
 /* Introspection: W, H, row_begin, row_end, which step kernel runs
- * (1 = fast streaming path, 0 = generic), and the number of step-kernel
- * launches enqueued so far. */
+ * (2 = bit-plane path, 1 = byte streaming path, 0 = generic), and the number
+ * of step-kernel launches enqueued so far. */
 int fhpg_info(fhpg_engine* e, int* width, int* height, int* row_begin, int* row_end,
               int* fast_path, uint64_t* step_launches);
 
 /* Testing aid: force the generic (one-thread-per-site) step kernel. */
 int fhpg_force_generic(fhpg_engine* e, int on);
+
+/* Step-kernel selection: 0 = automatic (bit-plane path when the table has a
+ * bit-sliced circuit — FHP-III — and W % 1024 == 0, else the byte streaming
+ * path when W allows it, else generic), 1 = byte paths only, 2 = generic.
+ * The resident state is converted between layouts on the device; results
+ * are identical on every path. */
+int fhpg_select_path(fhpg_engine* e, int path);
 
 #ifdef __cplusplus
 }

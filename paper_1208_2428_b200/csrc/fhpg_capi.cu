@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/fhpg.h"
+#include "../../include/fhpg_tables.h"
 #include "fhpg_common.cuh"
 #include "fhpg_kernels.cuh"
 
@@ -18,6 +19,15 @@ struct fhpg_engine {
   uint8_t* buf[2] = {nullptr, nullptr};  // (nrows + 4) * pitch each: halo, rows, halo, 2 spare
   int cur = 0;
   uint8_t* mask = nullptr;               // nrows * pitch, 0/1
+  // Bit-plane layout (fhpg_step_planes.cu): used while the table has a
+  // bit-sliced circuit and W allows it. `scratch` then holds a byte image of
+  // the state when `scratch_valid` (exact uploaded bytes until the first
+  // step, an unpacked copy afterwards).
+  bool planes = false;
+  bool table_planes = false;
+  int path_pref = 0;                     // 0 auto, 1 byte fast path, 2 generic
+  uint8_t* scratch = nullptr;            // nrows * pitch
+  bool scratch_valid = false;
   uint8_t* table = nullptr;              // 512 bytes
   uint64_t* zkeys = nullptr;             // [parity][purpose][W]
   unsigned long long* swaps = nullptr;
@@ -26,7 +36,6 @@ struct fhpg_engine {
   cudaStream_t own_stream = nullptr;
   bool table_set = false;
   bool normalized = true;                // state bit 7 == mask
-  bool force_generic = false;
   int num_sms = 148;
   uint64_t launches = 0;
   int64_t keys_step = -1;                // step whose column keys are in keys(step & 1)
@@ -98,6 +107,7 @@ void release(fhpg_engine* e) {
   cudaFree(e->buf[0]);
   cudaFree(e->buf[1]);
   cudaFree(e->mask);
+  cudaFree(e->scratch);
   cudaFree(e->table);
   cudaFree(e->zkeys);
   cudaFree(e->swaps);
@@ -126,7 +136,8 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
     e->nrows = re - rb;
     e->device = device;
     e->pitch = (static_cast<size_t>(W) + 15) / 16 * 16;
-    const size_t bytes = (static_cast<size_t>(e->nrows) + 4) * e->pitch;  // halos + 2 spare rows
+    // halo above, rows, halo below, 3 spare zero rows the streaming kernels may prefetch
+    const size_t bytes = (static_cast<size_t>(e->nrows) + 5) * e->pitch;
     for (int i = 0; i < 2; ++i) {
       ck(cudaMalloc(&e->buf[i], bytes), "cudaMalloc(state)");
       ck(cudaMemset(e->buf[i], 0, bytes), "cudaMemset(state)");
@@ -150,12 +161,76 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
   *out = e;
 }
 
+bool want_planes(const fhpg_engine* e) {
+  return e->table_set && e->table_planes && e->path_pref == 0 && fhpg::planes_ok(e->W);
+}
+
+void need_scratch(fhpg_engine* e) {
+  if (e->scratch) return;
+  ck(cudaMalloc(&e->scratch, static_cast<size_t>(e->nrows) * e->pitch), "cudaMalloc(scratch)");
+}
+
+// Byte image of the current state (device, local row 0, pitch e->pitch).
+uint8_t* bytes_view(fhpg_engine* e) {
+  if (!e->planes) return e->base(e->cur);
+  if (!e->scratch_valid) {
+    need_scratch(e);
+    fhpg::launch_unpack_planes(e->base(e->cur), e->scratch, e->pitch, e->W, e->nrows,
+                               e->num_sms, e->stream);
+    ck(cudaGetLastError(), "unpack launch");
+    e->scratch_valid = true;
+  }
+  return e->scratch;
+}
+
+// scratch (bytes) -> current plane buffer; plane 7 (obstacles, from the mask)
+// into both buffers. The step never writes plane 7.
+void pack_from_scratch(fhpg_engine* e) {
+  fhpg::launch_pack_planes(e->scratch, e->mask, e->base(e->cur), e->base(e->cur ^ 1), e->pitch,
+                           e->W, e->nrows, e->num_sms, e->stream);
+  ck(cudaGetLastError(), "pack launch");
+}
+
+// Put the resident state in the layout the table / path selection wants.
+void sync_layout(fhpg_engine* e) {
+  const bool want = want_planes(e);
+  if (want == e->planes) return;
+  if (want) {
+    need_scratch(e);
+    ck(cudaMemcpy2DAsync(e->scratch, e->pitch, e->base(e->cur), e->pitch, e->W, e->nrows,
+                         cudaMemcpyDeviceToDevice, e->stream), "layout copy");
+    e->scratch_valid = true;
+    pack_from_scratch(e);
+    e->planes = true;
+  } else {
+    const uint8_t* v = bytes_view(e);
+    ck(cudaMemcpy2DAsync(e->base(e->cur), e->pitch, v, e->pitch, e->W, e->nrows,
+                         cudaMemcpyDeviceToDevice, e->stream), "layout copy");
+    e->planes = false;
+    e->scratch_valid = false;
+    e->normalized = false;  // re-derived from the mask at the next step
+  }
+  ck(cudaStreamSynchronize(e->stream), "layout sync");
+}
+
+// Enqueue one step launch over rows [a.row_lo, a.row_hi) with the kernel the
+// layout selects.
+void launch_any(fhpg_engine* e, const fhpg::StepArgs& a) {
+  if (e->planes) {
+    e->launches += fhpg::launch_step_planes(a, e->num_sms, e->stream);
+    e->scratch_valid = false;
+  } else {
+    e->launches += fhpg::launch_step(a, e->num_sms, e->stream, e->path_pref == 2);
+  }
+  ck(cudaGetLastError(), "step launch");
+}
+
 void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64_t count) {
   using namespace fhpg;
   if (!e->table_set) invalid("collision table not set (fhpg_set_table)");
   if (thr > (1ull << 32)) invalid("force threshold must be <= 2^32");
   cudaStream_t st = e->stream;
-  if (!e->normalized) {
+  if (!e->planes && !e->normalized) {
     launch_apply_mask(e->base(e->cur), e->mask, e->pitch, e->W, e->nrows, st);
     ck(cudaGetLastError(), "apply_mask launch");
     e->normalized = true;
@@ -187,8 +262,7 @@ void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64
     }
     a.row_lo = 0;
     a.row_hi = e->nrows;
-    e->launches += launch_step(a, e->num_sms, st, e->force_generic);
-    ck(cudaGetLastError(), "step launch");
+    launch_any(e, a);
     e->cur ^= 1;
   }
   e->keys_step = -1;
@@ -203,7 +277,7 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
   if (thr > (1ull << 32)) invalid("force threshold must be <= 2^32");
   if (part != 0 && part != 1) invalid("part must be 0 (interior) or 1 (boundary rows)");
   cudaStream_t st = e->stream;
-  if (!e->normalized) {
+  if (!e->planes && !e->normalized) {
     launch_apply_mask(e->base(e->cur), e->mask, e->pitch, e->W, e->nrows, st);
     ck(cudaGetLastError(), "apply_mask launch");
     e->normalized = true;
@@ -241,8 +315,7 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
       b.kc_next = step_key(seed, kChirality, s + 1);
       b.kf_next = step_key(seed, kForcing, s + 1);
     }
-    e->launches += launch_step(b, e->num_sms, st, e->force_generic);
-    ck(cudaGetLastError(), "step launch");
+    launch_any(e, b);
   };
   if (part == 0) {
     if (interior) run(1, e->nrows - 1, true);
@@ -318,6 +391,11 @@ int fhpg_set_table(fhpg_engine* e, const uint8_t* t) {
     ck(cudaMemcpyAsync(e->table, t, 512, cudaMemcpyHostToDevice, e->stream), "table upload");
     ck(cudaStreamSynchronize(e->stream), "table upload sync");
     e->table_set = true;
+    // The bit-plane kernel evaluates FHP-III as a circuit (fhpg_planes_rules.cuh).
+    uint8_t fhp3[512];
+    fhpg_build_table(FHPG_RULES_FHP_III, fhp3);
+    e->table_planes = std::memcmp(t, fhp3, 512) == 0;
+    sync_layout(e);
   });
 }
 
@@ -330,8 +408,10 @@ int fhpg_set_obstacles(fhpg_engine* e, const uint8_t* mask, size_t stride) {
     // Raw bytes (nonzero = solid) go straight to the device mask.
     copy_rows_h2d(e->mask, e->pitch, mask, stride, e->W, e->nrows, e->stream);
     // Lattice::set_obstacle also sets / clears bit 7 of the node (lattice.cpp:25-29).
-    fhpg::launch_apply_mask(e->base(e->cur), e->mask, e->pitch, e->W, e->nrows, e->stream);
+    uint8_t* v = bytes_view(e);
+    fhpg::launch_apply_mask(v, e->mask, e->pitch, e->W, e->nrows, e->stream);
     ck(cudaGetLastError(), "apply_mask launch");
+    if (e->planes) pack_from_scratch(e);
     ck(cudaStreamSynchronize(e->stream), "mask sync");
   });
 }
@@ -342,9 +422,18 @@ int fhpg_upload(fhpg_engine* e, const uint8_t* state, size_t stride) {
     if (!state) invalid("null state");
     if (stride < static_cast<size_t>(e->W)) invalid("stride < width");
     DeviceGuard g(e->device);
-    copy_rows_h2d(e->base(e->cur), e->pitch, state, stride, e->W, e->nrows, e->stream);
+    if (e->planes) {
+      // The byte image stays exact until the first step; the planes take
+      // bit 7 from the mask like the reference's motion pass.
+      need_scratch(e);
+      copy_rows_h2d(e->scratch, e->pitch, state, stride, e->W, e->nrows, e->stream);
+      e->scratch_valid = true;
+      pack_from_scratch(e);
+    } else {
+      copy_rows_h2d(e->base(e->cur), e->pitch, state, stride, e->W, e->nrows, e->stream);
+      e->normalized = false;
+    }
     ck(cudaStreamSynchronize(e->stream), "upload sync");
-    e->normalized = false;
   });
 }
 
@@ -354,7 +443,7 @@ int fhpg_download(fhpg_engine* e, uint8_t* state, size_t stride) {
     if (!state) invalid("null state");
     if (stride < static_cast<size_t>(e->W)) invalid("stride < width");
     DeviceGuard g(e->device);
-    ck(cudaMemcpy2DAsync(state, stride, e->base(e->cur), e->pitch, e->W, e->nrows,
+    ck(cudaMemcpy2DAsync(state, stride, bytes_view(e), e->pitch, e->W, e->nrows,
                          cudaMemcpyDeviceToHost, e->stream),
        "cudaMemcpy2D D2H");
     ck(cudaStreamSynchronize(e->stream), "download sync");
@@ -367,7 +456,9 @@ int fhpg_init(fhpg_engine* e, uint64_t seed, double fill_density) {
     // lattice.cpp:58-60
     if (!(fill_density >= 0.0 && fill_density <= 1.0)) invalid("fill_density must be in [0,1]");
     DeviceGuard g(e->device);
-    fhpg::launch_init(e->base(e->cur), e->mask, e->pitch, e->W, e->nrows, e->row_begin, e->H,
+    if (e->planes) need_scratch(e);
+    uint8_t* target = e->planes ? e->scratch : e->base(e->cur);
+    fhpg::launch_init(target, e->mask, e->pitch, e->W, e->nrows, e->row_begin, e->H,
                       seed, fhpg::bernoulli_threshold(fill_density), e->stream);
     ck(cudaGetLastError(), "init launch");
     // Walls join the obstacle mask (init_impl calls set_obstacle on them).
@@ -376,6 +467,10 @@ int fhpg_init(fhpg_engine* e, uint64_t seed, double fill_density) {
       if (gr == 0 || gr == e->H - 1)
         ck(cudaMemsetAsync(e->mask + static_cast<size_t>(r) * e->pitch, 1, e->W, e->stream),
            "wall mask");
+    }
+    if (e->planes) {
+      e->scratch_valid = true;
+      pack_from_scratch(e);
     }
     ck(cudaStreamSynchronize(e->stream), "init sync");
     e->normalized = true;
@@ -440,7 +535,7 @@ int fhpg_reduce_global(fhpg_engine* e, int64_t* mass, int64_t* px, int64_t* py) 
     need(e);
     DeviceGuard g(e->device);
     ck(cudaMemsetAsync(e->acc, 0, sizeof(long long) * 3, e->stream), "acc reset");
-    fhpg::launch_reduce_global(e->base(e->cur), e->pitch, e->W, e->nrows, e->acc, e->stream);
+    fhpg::launch_reduce_global(bytes_view(e), e->pitch, e->W, e->nrows, e->acc, e->stream);
     ck(cudaGetLastError(), "reduce launch");
     long long h[3];
     ck(cudaMemcpyAsync(h, e->acc, sizeof h, cudaMemcpyDeviceToHost, e->stream), "acc read");
@@ -469,7 +564,7 @@ int fhpg_reduce_cells(fhpg_engine* e, int B, int32_t* nodes, int32_t* particles,
     long long* dx = reinterpret_cast<long long*>(static_cast<char*>(d) + n * 8);
     long long* dy = dx + n;
     ck(cudaMemsetAsync(d, 0, n * 24, e->stream), "cells reset");
-    fhpg::launch_reduce_cells(e->base(e->cur), e->pitch, e->W, e->nrows, e->row_begin, e->H, B,
+    fhpg::launch_reduce_cells(bytes_view(e), e->pitch, e->W, e->nrows, e->row_begin, e->H, B,
                               dn, dp, dx, dy, e->stream);
     ck(cudaGetLastError(), "cells launch");
     ck(cudaMemcpyAsync(nodes, dn, n * 4, cudaMemcpyDeviceToHost, e->stream), "cells read");
@@ -493,7 +588,7 @@ int fhpg_reduce_rows(fhpg_engine* e, int64_t* px, int32_t* fluid) {
     ck(cudaMallocAsync(&d, n * 12, e->stream), "cudaMallocAsync(rows)");
     long long* dx = static_cast<long long*>(d);
     int* df = reinterpret_cast<int*>(dx + n);
-    fhpg::launch_reduce_rows(e->base(e->cur), e->pitch, e->W, e->nrows, e->row_begin, e->H, dx,
+    fhpg::launch_reduce_rows(bytes_view(e), e->pitch, e->W, e->nrows, e->row_begin, e->H, dx,
                              df, e->stream);
     ck(cudaGetLastError(), "rows launch");
     ck(cudaMemcpyAsync(px + (lo - 1), dx + (lo - 1), (hi - lo) * 8, cudaMemcpyDeviceToHost, e->stream), "rows read");
@@ -524,7 +619,8 @@ int fhpg_info(fhpg_engine* e, int* width, int* height, int* row_begin, int* row_
     if (height) *height = e->H;
     if (row_begin) *row_begin = e->row_begin;
     if (row_end) *row_end = e->row_end;
-    if (fast_path) *fast_path = (!e->force_generic && fhpg::fast_path_ok(e->W)) ? 1 : 0;
+    if (fast_path)
+      *fast_path = e->planes ? 2 : (e->path_pref != 2 && fhpg::fast_path_ok(e->W)) ? 1 : 0;
     if (step_launches) *step_launches = e->launches;
   });
 }
@@ -532,7 +628,19 @@ int fhpg_info(fhpg_engine* e, int* width, int* height, int* row_begin, int* row_
 int fhpg_force_generic(fhpg_engine* e, int on) {
   return guarded([&] {
     need(e);
-    e->force_generic = on != 0;
+    DeviceGuard g(e->device);
+    e->path_pref = on ? 2 : 0;
+    sync_layout(e);
+  });
+}
+
+int fhpg_select_path(fhpg_engine* e, int path) {
+  return guarded([&] {
+    need(e);
+    if (path < 0 || path > 2) invalid("path must be 0 (auto), 1 (byte fast path) or 2 (generic)");
+    DeviceGuard g(e->device);
+    e->path_pref = path;
+    sync_layout(e);
   });
 }
 

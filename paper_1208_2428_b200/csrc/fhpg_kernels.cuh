@@ -46,6 +46,20 @@ int launch_step_fast(const StepArgs& a, int num_sms, cudaStream_t st);
 // Kernel selection for a lattice width.
 bool fast_path_ok(int W);
 
+// Bit-plane path (fhpg_step_planes.cu): rows hold 8 planes of W/8 bytes
+// (plane p: bit p of every node; bit j of word i = column 32 i + j).
+bool planes_ok(int W);  // W % 1024 == 0
+int planes_words_per_lane(int W);
+// One time step with the FHP-III circuit over rows [row_lo, row_hi).
+int launch_step_planes(const StepArgs& a, int num_sms, cudaStream_t st);
+// Bytes (rows 0..nrows-1 of src) -> planes in dst; plane 7 from the mask,
+// also written into dst_obst (the other ping-pong buffer).
+void launch_pack_planes(const uint8_t* src, const uint8_t* mask, uint8_t* dst, uint8_t* dst_obst,
+                        size_t pitch, int W, int nrows, int num_sms, cudaStream_t st);
+// Planes -> bytes (bit 7 from plane 7).
+void launch_unpack_planes(const uint8_t* src, uint8_t* dst, size_t pitch, int W, int nrows,
+                          int num_sms, cudaStream_t st);
+
 // One time step (motion -> collision -> forcing) over rows [row_lo,row_hi).
 // Returns the number of kernel launches enqueued.
 int launch_step(const StepArgs& a, int num_sms, cudaStream_t st, bool force_generic);

@@ -60,6 +60,7 @@ SIGNATURES = {
     "fhpg_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                             C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), u64p]),
     "fhpg_force_generic": (C.c_int, [C.c_void_p, C.c_int]),
+    "fhpg_select_path": (C.c_int, [C.c_void_p, C.c_int]),
     # include/fhpg_tables.h
     "fhpg_build_table": (C.c_int, [C.c_int, u8p]),
     "fhpg_validate_table": (C.c_int, [u8p, C.POINTER(C.c_int)]),
@@ -168,6 +169,19 @@ class Engine:
     @property
     def fast_path(self) -> bool:
         return bool(self._info()[4])
+
+    PATHS = {0: "generic", 1: "bytes", 2: "planes"}
+
+    @property
+    def path(self) -> str:
+        """Step kernel in use: "planes" (bit-plane circuit), "bytes" (byte
+        streaming LUT kernel) or "generic" (one thread per site)."""
+        return self.PATHS[self._info()[4]]
+
+    def select_path(self, path: str):
+        """"auto" (default), "bytes" (no bit-plane path) or "generic"."""
+        code = {"auto": 0, "bytes": 1, "generic": 2}[path]
+        _check(self.lib.fhpg_select_path(self.h, code))
 
     @property
     def step_launches(self) -> int:

@@ -1,0 +1,77 @@
+// Exhaustive check of the bit-sliced collision circuits used by the bit-plane
+// kernel (paper_1208_2428_b200/csrc/fhpg_planes_rules.cuh) against the
+// 512-entry tables (fhpg_tables.cpp): all 256 states (bit 7 = obstacle) x
+// both chiralities, 32 sites per word. Also checks that sites outside `dep`
+// do not read the chirality word and that `dep` is exactly "table outcome
+// depends on chirality". Exit status 0 = all rules match.
+//   g++ -std=c++17 -O1 -I include -I paper_1208_2428_b200/csrc \
+//       tools/planes_rules_check.cpp paper_1208_2428_b200/csrc/fhpg_tables.cpp
+#include <cstdint>
+#include <cstdio>
+
+#include "fhpg_planes_rules.cuh"
+#include "fhpg_tables.h"
+
+using namespace fhpg;
+
+struct Words {
+  uint32_t a[6], r, solid;
+};
+
+// Sites i = 32 w + j, state s = i & 255 (the word covers 32 consecutive states).
+static Words pack(int w) {
+  Words x{};
+  for (int j = 0; j < 32; ++j) {
+    const unsigned s = static_cast<unsigned>(w * 32 + j) & 255u;
+    for (int k = 0; k < 6; ++k) x.a[k] |= ((s >> k) & 1u) << j;
+    x.r |= ((s >> 6) & 1u) << j;
+    x.solid |= ((s >> 7) & 1u) << j;
+  }
+  return x;
+}
+
+template <typename Classify, typename Apply>
+static int check(const char* name, int variant, Classify classify, Apply apply) {
+  uint8_t t[512];
+  fhpg_build_table(variant, t);
+  int bad = 0, deps = 0;
+  for (int w = 0; w < 8; ++w) {
+    const Words x = pack(w);
+    const auto k = classify(x.a, x.r, x.solid);
+    uint32_t o0[6], o1[6], r0, r1;
+    apply(k, 0u, x.r, o0, r0);
+    apply(k, ~0u, x.r, o1, r1);
+    for (int j = 0; j < 32; ++j) {
+      const unsigned s = static_cast<unsigned>(w * 32 + j);
+      for (int c = 0; c < 2; ++c) {
+        const uint32_t* o = c ? o1 : o0;
+        const uint32_t rr = c ? r1 : r0;
+        unsigned got = ((rr >> j) & 1u) << 6 | (s & 0x80u);
+        for (int q = 0; q < 6; ++q) got |= ((o[q] >> j) & 1u) << q;
+        if (got != t[(c << 8) | s]) {
+          if (bad < 10) printf("%s: state %02x c=%d: got %02x want %02x\n", name, s, c, got, t[(c << 8) | s]);
+          ++bad;
+        }
+      }
+      const bool dep_t = t[s] != t[256 + s];
+      const bool dep_k = (k.dep >> j) & 1u;
+      deps += dep_k;
+      if (dep_t != dep_k) {
+        if (bad < 10) printf("%s: state %02x dep got %d want %d\n", name, s, dep_k, dep_t);
+        ++bad;
+      }
+    }
+  }
+  printf("%s: %s (%d dep states)\n", name, bad ? "MISMATCH" : "ok", deps);
+  return bad;
+}
+
+int main() {
+  int bad = 0;
+  bad += check("fhp3", FHPG_RULES_FHP_III,
+               [](const uint32_t* a, uint32_t r, uint32_t s) { return fhp3_classify(a, r, s); },
+               [](const Fhp3Class& k, uint32_t c, uint32_t r, uint32_t* o, uint32_t& orr) {
+                 fhp3_apply(k, c, r, o, orr);
+               });
+  return bad ? 1 : 0;
+}
