@@ -33,6 +33,7 @@
 // shared-memory ORs. Forcing (thr > 0) is resolved the same way on the
 // post-collision candidates (fluid, W set, E clear).
 #include <cstdint>
+#include <type_traits>
 
 #include "fhpg_common.cuh"
 #include "fhpg_kernels.cuh"
@@ -42,7 +43,7 @@ namespace fhpg {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kPWarps = 8;
+constexpr int kPWarps = 16;
 constexpr int kPThreads = kPWarps * 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -53,9 +54,20 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint2 lds64v(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ uint64_t lds64(uint32_t a) {
   uint64_t v;
   asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
@@ -63,6 +75,9 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
 }
 __device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
   asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v));
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w));
 }
 __device__ __forceinline__ void red_or(uint32_t a, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
@@ -73,227 +88,262 @@ __device__ __forceinline__ uint32_t top_bit(uint32_t m) {
   return p;
 }
 
-// NW consecutive words: vector loads / stores.
-template <int NW>
-__device__ __forceinline__ void ldv(const uint32_t* p, uint32_t (&v)[NW]) {
-  if constexpr (NW == 4) {
-    const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-  } else if constexpr (NW == 2) {
-    const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
-    v[0] = t.x; v[1] = t.y;
-  } else {
-    v[0] = __ldg(p);
-  }
+// mbarrier + bulk async copy (TMA engine, non-tensor form).
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
 template <int NW>
 __device__ __forceinline__ void stv(uint32_t* p, const uint32_t (&v)[NW]) {
-  if constexpr (NW == 4) {
-    __stcs(reinterpret_cast<uint4*>(p), make_uint4(v[0], v[1], v[2], v[3]));
-  } else if constexpr (NW == 2) {
+  if constexpr (NW == 2) {
     __stcs(reinterpret_cast<uint2*>(p), make_uint2(v[0], v[1]));
   } else {
     __stcs(p, v[0]);
   }
 }
 
-// A source row as loaded: 8 planes of NW words, plus 4 band-edge words for
-// the planes that shift (lane 0: word left of the band, lane 31: word right
-// of it).
-template <int NW>
-struct Raw {
-  uint32_t v[8][NW];
-  uint32_t e[4];
+// Geometry of a warp's smem: a ring of kSlots source rows. A slot holds the
+// 8 planes of the band, each as [16 B left edge chunk | band words | 16 B
+// right edge chunk] so that the +-1 column funnel shifts read the
+// neighbouring lane's (or band's) word straight from shared memory.
+template <int NW, bool FORCE>
+struct Geo {
+  static constexpr int kBandWords = 32 * NW;
+  static constexpr int kBandCols = 1024 * NW;
+  static constexpr int kPlane = 32 + 4 * kBandWords;
+  static constexpr int kSlot = 8 * kPlane;
+  static constexpr int kSlots = FORCE ? 4 : 5;
+  static constexpr int kList = 16 * kBandWords;   // walk list entries (uint4)
+  static constexpr int kOut = 4 * kBandWords;     // walk result words
+  static constexpr int kWarp = (kSlots * kSlot + kList + kOut + 8 * kSlots + 127) / 128 * 128;
+  static constexpr uint32_t kRowBytes = 8u * 4u * kBandWords + 4u * 16u;
 };
 
-// A source row after arrival processing: the planes as its three
-// destination rows pull them (rows s-1: n0, n1; s: c2, c5, c6, c7; s+1: p3, p4).
-template <int NW>
-struct Src {
-  uint32_t n0[NW], n1[NW], c2[NW], c5[NW], c6[NW], c7[NW], p3[NW], p4[NW];
-};
-
-struct Band {
+struct Lanes {
   int lane;
-  int WW;                 // words per plane row
-  int plane_words;        // = WW (offset between planes, in words)
-  int wlane;              // first word of this lane
-  int wedge;              // edge word this lane loads (lane 0: left, 31: right)
+  int WW;           // words per plane row (W / 32)
+  int w0;           // first word of the band
+  int wl, wr;       // first word of the left / right edge chunks (periodic)
 };
-
-// Shifted planes. L: out bit j = column x-1 (funnel with the previous word);
-// R: out bit j = column x+1 (funnel with the next word).
-template <int NW>
-__device__ __forceinline__ void shift_l(const uint32_t (&v)[NW], uint32_t edge, int lane,
-                                        uint32_t (&o)[NW]) {
-  const uint32_t up = __shfl_up_sync(kFull, v[NW - 1], 1);
-  const uint32_t prev = lane == 0 ? edge : up;
-  o[0] = __funnelshift_l(prev, v[0], 1);
-#pragma unroll
-  for (int i = 1; i < NW; ++i) o[i] = __funnelshift_l(v[i - 1], v[i], 1);
-}
-template <int NW>
-__device__ __forceinline__ void shift_r(const uint32_t (&v)[NW], uint32_t edge, int lane,
-                                        uint32_t (&o)[NW]) {
-  const uint32_t dn = __shfl_down_sync(kFull, v[0], 1);
-  const uint32_t next = lane == 31 ? edge : dn;
-#pragma unroll
-  for (int i = 0; i < NW - 1; ++i) o[i] = __funnelshift_r(v[i], v[i + 1], 1);
-  o[NW - 1] = __funnelshift_r(v[NW - 1], next, 1);
-}
-template <int NW>
-__device__ __forceinline__ void copy(const uint32_t (&v)[NW], uint32_t (&o)[NW]) {
-#pragma unroll
-  for (int i = 0; i < NW; ++i) o[i] = v[i];
-}
 
 // Planes that shift for a source row of global parity PS (pull offsets,
 // backends.cpp:64-73, with the destination row's parity q):
 //   PS = 0: plane 0 R (dest s-1, q=1), 2 L, 4 R (dest s+1, q=1), 5 R
 //   PS = 1: plane 1 L (dest s-1, q=0), 2 L, 3 L (dest s+1, q=0), 5 R
-template <int PS>
-__device__ __forceinline__ constexpr int edge_plane(int slot) {
-  return PS == 0 ? (slot == 0 ? 0 : slot == 1 ? 2 : slot == 2 ? 4 : 5)
-                 : (slot == 0 ? 1 : slot == 1 ? 2 : slot == 2 ? 3 : 5);
-}
-
-template <int NW, int PS>
-__device__ __forceinline__ void load_row(const uint8_t* row, const Band& b, Raw<NW>& r) {
-  const uint32_t* base = reinterpret_cast<const uint32_t*>(row);
+// Issue the bulk copies of source row `row` (local index) into `slot`
+// (called by one lane).
+template <int NW, bool FORCE>
+__device__ __forceinline__ void issue_row(const uint8_t* src, long long pitch, long long row,
+                                          int ps, const Lanes& L, uint32_t slot, uint32_t bar) {
+  using G = Geo<NW, FORCE>;
+  const uint8_t* r = src + row * pitch;
+  const size_t pb = static_cast<size_t>(L.WW) * 4;  // bytes per plane row
+  mbar_expect_tx(bar, G::kRowBytes);
 #pragma unroll
-  for (int p = 0; p < 8; ++p) ldv<NW>(base + p * b.plane_words + b.wlane, r.v[p]);
-#pragma unroll
-  for (int s = 0; s < 4; ++s) r.e[s] = __ldg(base + edge_plane<PS>(s) * b.plane_words + b.wedge);
-}
-
-template <int NW, int PS>
-__device__ __forceinline__ void arrive(const Raw<NW>& r, int lane, Src<NW>& s) {
-  if constexpr (PS == 0) {
-    shift_r<NW>(r.v[0], r.e[0], lane, s.n0);
-    copy<NW>(r.v[1], s.n1);
-    shift_l<NW>(r.v[2], r.e[1], lane, s.c2);
-    copy<NW>(r.v[3], s.p3);
-    shift_r<NW>(r.v[4], r.e[2], lane, s.p4);
-    shift_r<NW>(r.v[5], r.e[3], lane, s.c5);
+  for (int p = 0; p < 8; ++p)
+    bulk_g2s(slot + p * G::kPlane + 16, r + p * pb + L.w0 * 4, 4 * G::kBandWords, bar);
+  const int pl0 = ps ? 1 : 0, pl3 = ps ? 3 : 4;
+  // left chunks for L shifts, right chunks for R shifts
+  if (ps) {
+    bulk_g2s(slot + pl0 * G::kPlane, r + pl0 * pb + L.wl * 4, 16, bar);
+    bulk_g2s(slot + pl3 * G::kPlane, r + pl3 * pb + L.wl * 4, 16, bar);
   } else {
-    copy<NW>(r.v[0], s.n0);
-    shift_l<NW>(r.v[1], r.e[0], lane, s.n1);
-    shift_l<NW>(r.v[2], r.e[1], lane, s.c2);
-    shift_l<NW>(r.v[3], r.e[2], lane, s.p3);
-    copy<NW>(r.v[4], s.p4);
-    shift_r<NW>(r.v[5], r.e[3], lane, s.c5);
+    bulk_g2s(slot + pl0 * G::kPlane + 16 + 4 * G::kBandWords, r + pl0 * pb + L.wr * 4, 16, bar);
+    bulk_g2s(slot + pl3 * G::kPlane + 16 + 4 * G::kBandWords, r + pl3 * pb + L.wr * 4, 16, bar);
   }
-  copy<NW>(r.v[6], s.c6);
-  copy<NW>(r.v[7], s.c7);
+  bulk_g2s(slot + 2 * G::kPlane, r + 2 * pb + L.wl * 4, 16, bar);
+  bulk_g2s(slot + 5 * G::kPlane + 16 + 4 * G::kBandWords, r + 5 * pb + L.wr * 4, 16, bar);
+}
+
+// Plane words of this lane from a slot: aligned, or shifted by one column.
+template <int NW>
+__device__ __forceinline__ void rd_al(uint32_t a, uint32_t (&o)[NW]) {
+  if constexpr (NW == 2) {
+    const uint2 v = lds64v(a);
+    o[0] = v.x;
+    o[1] = v.y;
+  } else {
+    o[0] = lds32(a);
+  }
+}
+// L: out bit j = column x-1 (funnel with the previous word).
+template <int NW>
+__device__ __forceinline__ void rd_shl(uint32_t a, uint32_t (&o)[NW]) {
+  uint32_t v[NW];
+  rd_al<NW>(a, v);
+  const uint32_t prev = lds32(a - 4);
+  o[0] = __funnelshift_l(prev, v[0], 1);
+#pragma unroll
+  for (int i = 1; i < NW; ++i) o[i] = __funnelshift_l(v[i - 1], v[i], 1);
+}
+// R: out bit j = column x+1 (funnel with the next word).
+template <int NW>
+__device__ __forceinline__ void rd_shr(uint32_t a, uint32_t (&o)[NW]) {
+  uint32_t v[NW];
+  rd_al<NW>(a, v);
+  const uint32_t next = lds32(a + 4 * NW);
+#pragma unroll
+  for (int i = 0; i < NW - 1; ++i) o[i] = __funnelshift_r(v[i], v[i + 1], 1);
+  o[NW - 1] = __funnelshift_r(v[NW - 1], next, 1);
 }
 
 // Balanced walk over the set bits of the warp's NW * 32 mask words (word
-// i = lane * NW + w <-> band word i). The total T is split into 32 equal
-// contiguous slices; each lane finds the start of its slice (binary search
-// over the lanes' inclusive counts, then a popcount scan) and visits its
-// sites two at a time. fn(i0, j0, i1, j1, has1) handles two sites (word
-// index, bit) and returns the bits to OR into out[i] as (b0, b1).
+// i = lane * NW + w <-> band word i, bit j <-> column 32 i + j of the band).
+// The warp's nonzero words go to a list {mask, word, sites before it}; the
+// T sites are split into 32 equal contiguous slices; each lane finds its
+// first word (binary search over the lanes' counts), skips the sites before
+// its slice and visits its sites two at a time, advancing through the list
+// (no empty words on it). fn(col0, col1, has1) returns the two result bits,
+// ORed into the result words (osm) bit by bit. Returns T.
 template <int NW, typename Fn>
-__device__ __forceinline__ void balanced_walk(const uint32_t (&m)[NW], uint32_t msm, int lane,
-                                              Fn&& fn) {
-  int cnt = 0;
+__device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint32_t osm, int lane,
+                                    Fn&& fn) {
+  int cnt = 0, nz = 0;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) cnt += __popc(m[w]);
-  int incl = cnt;
+  for (int w = 0; w < NW; ++w) {
+    cnt += __popc(m[w]);
+    nz += m[w] != 0u;
+  }
+  const int packed = cnt | (nz << 16);
+  int incl = packed;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const int v = __shfl_up_sync(kFull, incl, d);
     if (lane >= d) incl += v;
   }
-  const int T = __shfl_sync(kFull, incl, 31);
-  if (T == 0) return;
+  const int T = __shfl_sync(kFull, incl, 31) & 0xFFFF;
+  if (T == 0) return 0;
+  const int excl = incl - packed;
+  {
+    int q = excl >> 16, c = excl & 0xFFFF;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      if (m[w]) {
+        sts128(lsm + q * 16, m[w], static_cast<uint32_t>(lane * NW + w), static_cast<uint32_t>(c), 0u);
+        ++q;
+        c += __popc(m[w]);
+      }
+      sts32(osm + (lane * NW + w) * 4, 0u);
+    }
+  }
+  __syncwarp();
   const int s = (lane * T) >> 5;
   const int e = ((lane + 1) * T) >> 5;
+  // owner lane of site s: last lane whose exclusive count is <= s
+  const int icnt = incl & 0xFFFF;
   int o = 0;
 #pragma unroll
   for (int step = 16; step; step >>= 1) {
-    const int v = __shfl_sync(kFull, incl, o + step - 1);
+    const int v = __shfl_sync(kFull, icnt, o + step - 1);
     if (v <= s) o += step;
   }
-  const int excl_o = __shfl_sync(kFull, incl - cnt, o);
-  if (s >= e) return;
-  int k = s - excl_o;
-  uint32_t i = static_cast<uint32_t>(o * NW);
-  uint32_t mask = lds32(msm + i * 4);
-  for (;;) {
-    const int c = __popc(mask);
-    if (k < c) break;
-    k -= c;
-    ++i;
-    mask = lds32(msm + i * 4);
-  }
-  for (; k > 0; --k) mask ^= 1u << top_bit(mask);
-  auto next = [&](uint32_t& wi, uint32_t& bj) {
-    while (mask == 0u) {
-      ++i;
-      mask = lds32(msm + i * 4);
+  const int o_excl = __shfl_sync(kFull, excl, o);
+  if (s < e) {
+    int q = o_excl >> 16;
+    uint4 en = lds128(lsm + q * 16);
+    if (NW > 1 && s >= static_cast<int>(en.z) + __popc(en.x)) {
+      ++q;
+      en = lds128(lsm + q * 16);
     }
-    bj = top_bit(mask);
-    mask ^= 1u << bj;
-    wi = i;
-  };
-  for (int it = s; it < e; it += 2) {
-    uint32_t i0, j0, i1 = 0, j1 = 0;
-    next(i0, j0);
-    const bool has1 = it + 1 < e;
-    if (has1) next(i1, j1);
-    fn(i0, j0, i1, j1, has1);
+    uint32_t mask = en.x;
+    uint32_t base = en.y * 32u;
+    for (int k = s - static_cast<int>(en.z); k > 0; --k) mask ^= 1u << top_bit(mask);
+    auto next = [&](uint32_t& col) {
+      if (mask == 0u) {
+        ++q;
+        const uint4 n = lds128(lsm + q * 16);
+        mask = n.x;
+        base = n.y * 32u;
+      }
+      const uint32_t j = top_bit(mask);
+      mask ^= 1u << j;
+      col = base + j;
+    };
+    for (int it = s; it < e; it += 2) {
+      uint32_t c0, c1 = 0;
+      next(c0);
+      const bool has1 = it + 1 < e;
+      if (has1) next(c1);
+      uint32_t b0, b1;
+      fn(c0, c1, has1, b0, b1);
+      red_or(osm + (c0 >> 5) * 4u, b0 << (c0 & 31u));
+      red_or(osm + (c1 >> 5) * 4u, b1 << (c1 & 31u));
+    }
   }
+  __syncwarp();
+  return T;
 }
 
 template <int NW, bool FORCE>
 struct Ctx {
   uint32_t kc;      // smem: chirality keys of the band (8 B per column)
   uint32_t kf;      // smem: forcing keys of the band
-  uint32_t msm;     // smem: warp's mask words [32 * NW]
-  uint32_t osm;     // smem: warp's result words [32 * NW]
+  uint32_t lsm;     // smem: walk list
+  uint32_t osm;     // smem: walk result words
   uint64_t thr;
 };
 
-// One destination row r (global parity Q is implicit in the Src planes).
-template <int NW, bool FORCE>
-__device__ __forceinline__ void dest_row(const Src<NW>& Pm, const Src<NW>& Pc, const Src<NW>& Pn,
+// One destination row. sm, sc, sn: this lane's word address inside plane 0
+// of the slots of rows r-1, r, r+1; Q = global parity of r.
+template <int NW, bool FORCE, int Q>
+__device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
                                          const Ctx<NW, FORCE>& cx, int lane, uint32_t y,
                                          uint32_t* out_row, int plane_words, unsigned& swaps) {
+  using G = Geo<NW, FORCE>;
+  constexpr int P = G::kPlane;
+  uint32_t a0[NW], a1[NW], a2[NW], a3[NW], a4[NW], a5[NW], rr[NW], so[NW];
+  // Pull sources (backends.cpp:64-73): k0 (x+q, r+1), k1 (x+q-1, r+1),
+  // k2 (x-1, r), k3 (x+q-1, r-1), k4 (x+q, r-1), k5 (x+1, r).
+  if (Q) rd_shr<NW>(sn + 0 * P, a0); else rd_al<NW>(sn + 0 * P, a0);
+  if (Q) rd_al<NW>(sn + 1 * P, a1); else rd_shl<NW>(sn + 1 * P, a1);
+  rd_shl<NW>(sc + 2 * P, a2);
+  if (Q) rd_al<NW>(sm + 3 * P, a3); else rd_shl<NW>(sm + 3 * P, a3);
+  if (Q) rd_shr<NW>(sm + 4 * P, a4); else rd_al<NW>(sm + 4 * P, a4);
+  rd_shr<NW>(sc + 5 * P, a5);
+  rd_al<NW>(sc + 6 * P, rr);
+  rd_al<NW>(sc + 7 * P, so);
   Fhp3Class K[NW];
   uint32_t dep[NW];
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
-    const uint32_t a[6] = {Pn.n0[w], Pn.n1[w], Pc.c2[w], Pm.p3[w], Pm.p4[w], Pc.c5[w]};
-    K[w] = fhp3_classify(a, Pc.c6[w], Pc.c7[w]);
+    const uint32_t a[6] = {a0[w], a1[w], a2[w], a3[w], a4[w], a5[w]};
+    K[w] = fhp3_classify(a, rr[w], so[w]);
     dep[w] = K[w].dep;
   }
-  // Stage masks, clear results.
-  const uint32_t mine = static_cast<uint32_t>(lane * NW) * 4u;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    sts32(cx.msm + mine + w * 4, dep[w]);
-    sts32(cx.osm + mine + w * 4, 0u);
-  }
-  __syncwarp();
   // Chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y)
   // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76).
-  balanced_walk<NW>(dep, cx.msm, lane, [&](uint32_t i0, uint32_t j0, uint32_t i1, uint32_t j1,
-                                           bool has1) {
-    const uint64_t k0 = lds64(cx.kc + (i0 * 32u + j0) * 8u);
-    const uint64_t k1 = lds64(cx.kc + (i1 * 32u + j1) * 8u);
-    const uint32_t b0 = fin64_bit0(k0 + y);
-    const uint32_t b1 = fin64_bit0(k1 + y) & (has1 ? 1u : 0u);
-    red_or(cx.osm + i0 * 4u, b0 << j0);
-    red_or(cx.osm + i1 * 4u, b1 << j1);
+  const int T = walk<NW>(dep, cx.lsm, cx.osm, lane,
+                         [&](uint32_t c0, uint32_t c1, bool has1, uint32_t& b0, uint32_t& b1) {
+    const uint64_t k0 = lds64(cx.kc + c0 * 8u);
+    const uint64_t k1 = lds64(cx.kc + c1 * 8u);
+    b0 = fin64_bit0(k0 + y);
+    b1 = fin64_bit0(k1 + y) & (has1 ? 1u : 0u);
   });
-  __syncwarp();
   uint32_t o[NW][7];
+  const uint32_t mine = cx.osm + lane * NW * 4;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
-    const uint32_t c = lds32(cx.osm + mine + w * 4);
+    const uint32_t c = T ? lds32(mine + w * 4) : 0u;
     uint32_t oo[6], orr;
-    fhp3_apply(K[w], c, Pc.c6[w], oo, orr);
+    fhp3_apply(K[w], c, rr[w], oo, orr);
 #pragma unroll
     for (int p = 0; p < 6; ++p) o[w][p] = oo[p];
     o[w][6] = orr;
@@ -302,33 +352,24 @@ __device__ __forceinline__ void dest_row(const Src<NW>& Pm, const Src<NW>& Pc, c
     // step.cpp:79-88: fluid, W (bit 5) set, E (bit 2) clear after collision.
     uint32_t f[NW];
 #pragma unroll
-    for (int w = 0; w < NW; ++w) f[w] = ~Pc.c7[w] & o[w][5] & ~o[w][2];
-    __syncwarp();
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      sts32(cx.msm + mine + w * 4, f[w]);
-      sts32(cx.osm + mine + w * 4, 0u);
-    }
-    __syncwarp();
-    balanced_walk<NW>(f, cx.msm, lane, [&](uint32_t i0, uint32_t j0, uint32_t i1, uint32_t j1,
-                                           bool has1) {
-      const uint64_t k0 = lds64(cx.kf + (i0 * 32u + j0) * 8u);
-      const uint64_t k1 = lds64(cx.kf + (i1 * 32u + j1) * 8u);
-      const uint32_t b0 = (fin64(k0 + y) >> 32) < cx.thr ? 1u : 0u;
-      const uint32_t b1 = has1 && (fin64(k1 + y) >> 32) < cx.thr ? 1u : 0u;
-      red_or(cx.osm + i0 * 4u, b0 << j0);
-      red_or(cx.osm + i1 * 4u, b1 << j1);
+    for (int w = 0; w < NW; ++w) f[w] = ~so[w] & o[w][5] & ~o[w][2];
+    const int TF = walk<NW>(f, cx.lsm, cx.osm, lane,
+                            [&](uint32_t c0, uint32_t c1, bool has1, uint32_t& b0, uint32_t& b1) {
+      const uint64_t k0 = lds64(cx.kf + c0 * 8u);
+      const uint64_t k1 = lds64(cx.kf + c1 * 8u);
+      b0 = (fin64(k0 + y) >> 32) < cx.thr ? 1u : 0u;
+      b1 = has1 && (fin64(k1 + y) >> 32) < cx.thr ? 1u : 0u;
     });
-    __syncwarp();
+    if (TF) {
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      const uint32_t acc = lds32(cx.osm + mine + w * 4);
-      o[w][5] ^= acc;
-      o[w][2] ^= acc;
-      swaps += __popc(acc);
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t acc = lds32(mine + w * 4);
+        o[w][5] ^= acc;
+        o[w][2] ^= acc;
+        swaps += __popc(acc);
+      }
     }
   }
-  __syncwarp();  // the next row restages msm / osm
 #pragma unroll
   for (int p = 0; p < 7; ++p) {
     uint32_t v[NW];
@@ -339,64 +380,79 @@ __device__ __forceinline__ void dest_row(const Src<NW>& Pm, const Src<NW>& Pc, c
 }
 
 template <int NW, bool FORCE, int Q0>
-__device__ __forceinline__ void run_segment(const StepArgs& a, const Band& b,
-                                            const Ctx<NW, FORCE>& cx, int r_begin, int r_end,
-                                            unsigned& swaps) {
-  constexpr int Q1 = Q0 ^ 1;
+__device__ __forceinline__ void run_segment(const StepArgs& a, const Lanes& L, uint32_t ring,
+                                            uint32_t bars, const Ctx<NW, FORCE>& cx, int r_begin,
+                                            int r_end, unsigned& swaps) {
+  using G = Geo<NW, FORCE>;
   const long long pitch = static_cast<long long>(a.pitch);
-  const uint8_t* src = a.src;
-  // Rows r-1 (parity Q1), r (Q0), r+1 (Q1) arrive; r+2 (Q0), r+3 (Q1) in flight.
-  Src<NW> Sm, Sc, Sn;
-  {
-    Raw<NW> t;
-    load_row<NW, Q1>(src + (r_begin - 1) * pitch, b, t);
-    arrive<NW, Q1>(t, b.lane, Sm);
-    load_row<NW, Q0>(src + r_begin * pitch, b, t);
-    arrive<NW, Q0>(t, b.lane, Sc);
-    load_row<NW, Q1>(src + (r_begin + 1) * pitch, b, t);
-    arrive<NW, Q1>(t, b.lane, Sn);
-  }
-  Raw<NW> R0, R1;  // rows r+2 (parity Q0) and r+3 (parity Q1)
-  // Only rows up to r_end are needed (a spare zero row follows the bottom halo).
-  if (r_begin + 2 <= r_end + 1) load_row<NW, Q0>(src + (r_begin + 2) * pitch, b, R0);
-  if (r_begin + 3 <= r_end) load_row<NW, Q1>(src + (r_begin + 3) * pitch, b, R1);
+  const int first = r_begin - 1;          // source rows first .. r_end
+  const int last = r_end;
+  const uint32_t lane_off = 16u + L.lane * NW * 4u;
+  auto slot_of = [&](int row) { return static_cast<uint32_t>((row - first) % G::kSlots); };
+  auto issue = [&](int row) {
+    if (L.lane == 0) {
+      const uint32_t k = slot_of(row);
+      issue_row<NW, FORCE>(a.src, pitch, row, static_cast<int>((a.row0 + row) & 1), L,
+                           ring + k * G::kSlot, bars + k * 8u);
+    }
+  };
+  auto wait = [&](int row) {
+    const uint32_t k = slot_of(row);
+    mbar_wait(bars + k * 8u, static_cast<uint32_t>(((row - first) / G::kSlots) & 1));
+  };
+  const int pro = min(last, first + G::kSlots - 1);
+  for (int row = first; row <= pro; ++row) issue(row);
+  wait(first);
+  wait(first + 1);
   const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
-  uint32_t* out = reinterpret_cast<uint32_t*>(a.dst + r_begin * pitch) + b.wlane;
+  uint32_t* out = reinterpret_cast<uint32_t*>(a.dst + r_begin * pitch) + L.w0 + L.lane * NW;
   const long long pw = pitch / 4;
+  auto one = [&](int r, auto qc) {
+    constexpr int Q = decltype(qc)::value;
+    wait(r + 1);
+    dest_row<NW, FORCE, Q>(ring + slot_of(r - 1) * G::kSlot + lane_off,
+                           ring + slot_of(r) * G::kSlot + lane_off,
+                           ring + slot_of(r + 1) * G::kSlot + lane_off, cx, L.lane, y0 + r, out,
+                           L.WW, swaps);
+    out += pw;
+    // Slot of row r-1 is free once every lane has read it.
+    __syncwarp();
+    if (r - 1 + G::kSlots <= last) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(r - 1 + G::kSlots);
+    }
+  };
   int r = r_begin;
-  // Two rows per iteration so that every parity is a compile-time constant.
-  // Spare zero rows below the bottom halo make the over-prefetch safe.
   for (; r + 2 <= r_end; r += 2) {
-    dest_row<NW, FORCE>(Sm, Sc, Sn, cx, b.lane, y0 + r, out, b.plane_words, swaps);
-    out += pw;
-    Sm = Sc;
-    Sc = Sn;
-    arrive<NW, Q0>(R0, b.lane, Sn);
-    if (r + 4 <= r_end) load_row<NW, Q0>(src + (r + 4) * pitch, b, R0);
-    dest_row<NW, FORCE>(Sm, Sc, Sn, cx, b.lane, y0 + r + 1, out, b.plane_words, swaps);
-    out += pw;
-    Sm = Sc;
-    Sc = Sn;
-    arrive<NW, Q1>(R1, b.lane, Sn);
-    if (r + 5 <= r_end) load_row<NW, Q1>(src + (r + 5) * pitch, b, R1);
+    one(r, std::integral_constant<int, Q0>{});
+    one(r + 1, std::integral_constant<int, Q0 ^ 1>{});
   }
-  if (r < r_end) dest_row<NW, FORCE>(Sm, Sc, Sn, cx, b.lane, y0 + r, out, b.plane_words, swaps);
+  if (r < r_end) one(r, std::integral_constant<int, Q0>{});
 }
 
 template <int NW, bool FORCE>
 __global__ void __launch_bounds__(kPThreads, 1) step_planes_kernel(StepArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  using G = Geo<NW, FORCE>;
+  extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
-  constexpr int kBandCols = NW * 1024;
   const int warp = threadIdx.x >> 5;
   const int band_group = blockIdx.x % a.nbands_groups;
   const int seg_group = blockIdx.x / a.nbands_groups;
-  const int cta_cols = a.bpc * kBandCols;
+  const int cta_cols = a.bpc * G::kBandCols;
   const int cta_x0 = band_group * cta_cols;
-  // smem: chirality keys [cta_cols], forcing keys [cta_cols], per warp 2 x 32 NW words.
+  // smem: chirality keys [cta_cols], forcing keys [cta_cols], then per warp
+  // the row ring, the walk list and results, the ring's mbarriers.
   const uint32_t kc_base = sbase;
   const uint32_t kf_base = sbase + cta_cols * 8;
-  const uint32_t warp_base = sbase + (FORCE ? 2 : 1) * cta_cols * 8 + warp * (2 * 32 * NW * 4);
+  const uint32_t wbase = sbase + (FORCE ? 2 : 1) * cta_cols * 8 + warp * G::kWarp;
+  const uint32_t ring = wbase;
+  const uint32_t lsm = ring + G::kSlots * G::kSlot;
+  const uint32_t osm = lsm + G::kList;
+  const uint32_t bars = osm + G::kOut;
+  if ((threadIdx.x & 31) == 0) {
+    for (int k = 0; k < G::kSlots; ++k) mbar_init(bars + k * 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int c = threadIdx.x; c < cta_cols; c += blockDim.x) {
     sts64(kc_base + c * 8, a.zc[cta_x0 + c]);
     if (FORCE) sts64(kf_base + c * 8, a.zf[cta_x0 + c]);
@@ -418,46 +474,45 @@ __global__ void __launch_bounds__(kPThreads, 1) step_planes_kernel(StepArgs a) {
   if (warp >= a.bpc * a.spc || band >= a.nbands || r_begin >= a.row_hi) return;  // whole warp
   const int r_end = min(a.row_hi, r_begin + a.seg_rows);
 
-  Band b;
-  b.lane = threadIdx.x & 31;
-  b.WW = a.W >> 5;
-  b.plane_words = a.W >> 5;
-  const int w0 = band * 32 * NW;
-  b.wlane = w0 + b.lane * NW;
-  b.wedge = b.lane == 0 ? (w0 == 0 ? b.WW - 1 : w0 - 1)
-                        : (b.lane == 31 ? (w0 + 32 * NW == b.WW ? 0 : w0 + 32 * NW) : b.wlane);
+  Lanes L;
+  L.lane = threadIdx.x & 31;
+  L.WW = a.W >> 5;
+  L.w0 = band * G::kBandWords;
+  L.wl = L.w0 == 0 ? L.WW - 4 : L.w0 - 4;
+  L.wr = L.w0 + G::kBandWords == L.WW ? 0 : L.w0 + G::kBandWords;
   Ctx<NW, FORCE> cx;
-  cx.kc = kc_base + bic * kBandCols * 8;
-  cx.kf = kf_base + bic * kBandCols * 8;
-  cx.msm = warp_base;
-  cx.osm = warp_base + 32 * NW * 4;
+  cx.kc = kc_base + bic * G::kBandCols * 8;
+  cx.kf = kf_base + bic * G::kBandCols * 8;
+  cx.lsm = lsm;
+  cx.osm = osm;
   cx.thr = a.thr;
   unsigned swaps = 0;
   if ((a.row0 + r_begin) & 1)
-    run_segment<NW, FORCE, 1>(a, b, cx, r_begin, r_end, swaps);
+    run_segment<NW, FORCE, 1>(a, L, ring, bars, cx, r_begin, r_end, swaps);
   else
-    run_segment<NW, FORCE, 0>(a, b, cx, r_begin, r_end, swaps);
+    run_segment<NW, FORCE, 0>(a, L, ring, bars, cx, r_begin, r_end, swaps);
   if (FORCE) {
     unsigned long long s = swaps;
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-    if (b.lane == 0 && s) atomicAdd(a.swaps, s);
+    if (L.lane == 0 && s) atomicAdd(a.swaps, s);
   }
 }
 
 template <int NW, bool FORCE>
 int smem_bytes(int bpc) {
-  return (FORCE ? 2 : 1) * bpc * NW * 1024 * 8 + kPWarps * 2 * 32 * NW * 4;
+  using G = Geo<NW, FORCE>;
+  return (FORCE ? 2 : 1) * bpc * G::kBandCols * 8 + kPWarps * G::kWarp;
 }
 
 template <int NW, bool FORCE>
 void launch_nw(StepArgs a, int num_sms, cudaStream_t st) {
-  constexpr int kBandCols = NW * 1024;
+  using G = Geo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
-  a.nbands = a.W / kBandCols;
-  // Bands per CTA: all of a row's bands when they fit (edge words then come
-  // from the same SM's recent loads), within the shared-memory budget.
+  a.nbands = a.W / G::kBandCols;
+  // Bands per CTA: as many as the shared-memory budget allows (the column
+  // keys of every band a CTA covers are staged).
   int bpc = a.nbands < kPWarps ? a.nbands : kPWarps;
-  while (bpc > 1 && smem_bytes<NW, FORCE>(bpc) > 200 * 1024) bpc >>= 1;
+  while (bpc > 1 && smem_bytes<NW, FORCE>(bpc) > 227 * 1024) bpc >>= 1;
   while (kPWarps % bpc) --bpc;
   a.bpc = bpc;
   a.spc = kPWarps / bpc;
@@ -465,7 +520,7 @@ void launch_nw(StepArgs a, int num_sms, cudaStream_t st) {
   int seg_groups = num_sms / a.nbands_groups;
   if (seg_groups < 1) seg_groups = 1;
   int seg = (rows + seg_groups * a.spc - 1) / (seg_groups * a.spc);
-  if (seg < 2) seg = 2;
+  if (seg < 1) seg = 1;
   a.seg_rows = seg;
   const int nseg = (rows + seg - 1) / seg;
   seg_groups = (nseg + a.spc - 1) / a.spc;
