@@ -27,6 +27,7 @@ struct fhpg_engine {
   bool table_planes = false;
   int path_pref = 0;                     // 0 auto, 1 byte fast path, 2 generic
   uint8_t* scratch = nullptr;            // nrows * pitch
+  alignas(64) unsigned char tmap[2][128];  // TMA descriptors of buf[0], buf[1] (planes)
   bool scratch_valid = false;
   uint8_t* table = nullptr;              // 512 bytes
   uint64_t* zkeys = nullptr;             // [parity][purpose][W]
@@ -135,12 +136,16 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
     e->row_end = re;
     e->nrows = re - rb;
     e->device = device;
-    e->pitch = (static_cast<size_t>(W) + 15) / 16 * 16;
+    // Room for the bit-plane rows (W + 256 bytes) when the width allows them.
+    e->pitch = (static_cast<size_t>(W) + 15) / 16 * 16 + (fhpg::planes_ok(W) ? 256 : 0);
     // halo above, rows, halo below, 3 spare zero rows the streaming kernels may prefetch
     const size_t bytes = (static_cast<size_t>(e->nrows) + 5) * e->pitch;
     for (int i = 0; i < 2; ++i) {
       ck(cudaMalloc(&e->buf[i], bytes), "cudaMalloc(state)");
       ck(cudaMemset(e->buf[i], 0, bytes), "cudaMemset(state)");
+      if (fhpg::planes_ok(W) &&
+          !fhpg::make_planes_map(e->tmap[i], e->buf[i], W, e->pitch, e->nrows + 5))
+        throw Failure{FHPG_ERUNTIME, "cuTensorMapEncodeTiled failed"};
     }
     ck(cudaMalloc(&e->mask, static_cast<size_t>(e->nrows) * e->pitch), "cudaMalloc(mask)");
     ck(cudaMemset(e->mask, 0, static_cast<size_t>(e->nrows) * e->pitch), "cudaMemset(mask)");
@@ -217,7 +222,8 @@ void sync_layout(fhpg_engine* e) {
 // layout selects.
 void launch_any(fhpg_engine* e, const fhpg::StepArgs& a) {
   if (e->planes) {
-    e->launches += fhpg::launch_step_planes(a, e->num_sms, e->stream);
+    const int which = a.src == e->base(0) ? 0 : 1;
+    e->launches += fhpg::launch_step_planes(a, e->tmap[which], e->num_sms, e->stream);
     e->scratch_valid = false;
   } else {
     e->launches += fhpg::launch_step(a, e->num_sms, e->stream, e->path_pref == 2);
@@ -607,7 +613,7 @@ int fhpg_halo(fhpg_engine* e, void** send_top, void** send_bottom, void** recv_t
     if (send_bottom) *send_bottom = b + static_cast<size_t>(e->nrows - 1) * e->pitch;
     if (recv_top) *recv_top = b - e->pitch;
     if (recv_bottom) *recv_bottom = b + static_cast<size_t>(e->nrows) * e->pitch;
-    if (row_bytes) *row_bytes = static_cast<size_t>(e->W);
+    if (row_bytes) *row_bytes = e->planes ? fhpg::planes_row_bytes(e->W) : static_cast<size_t>(e->W);
   });
 }
 

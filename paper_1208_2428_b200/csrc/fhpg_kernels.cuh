@@ -46,12 +46,18 @@ int launch_step_fast(const StepArgs& a, int num_sms, cudaStream_t st);
 // Kernel selection for a lattice width.
 bool fast_path_ok(int W);
 
-// Bit-plane path (fhpg_step_planes.cu): rows hold 8 planes of W/8 bytes
-// (plane p: bit p of every node; bit j of word i = column 32 i + j).
+// Bit-plane path (fhpg_step_planes.cu): rows hold 8 planes (plane p: bit p
+// of every node; bit j of word i = column 32 i + j), each W/32 words plus 4
+// periodic-wrap pad words on either side: planes_row_bytes(W) = W + 256.
 bool planes_ok(int W);  // W % 1024 == 0
 int planes_words_per_lane(int W);
-// One time step with the FHP-III circuit over rows [row_lo, row_hi).
-int launch_step_planes(const StepArgs& a, int num_sms, cudaStream_t st);
+size_t planes_row_bytes(int W);
+// TMA descriptor (CUtensorMap, 64-byte aligned, 128 bytes) of a plane buffer
+// whose row 0 is at `buffer` (the top halo row), `rows` rows.
+bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows);
+// One time step with the FHP-III circuit over rows [row_lo, row_hi);
+// tmap_src describes the buffer a.src lives in.
+int launch_step_planes(const StepArgs& a, const void* tmap_src, int num_sms, cudaStream_t st);
 // Bytes (rows 0..nrows-1 of src) -> planes in dst; plane 7 from the mask,
 // also written into dst_obst (the other ping-pong buffer).
 void launch_pack_planes(const uint8_t* src, const uint8_t* mask, uint8_t* dst, uint8_t* dst_obst,

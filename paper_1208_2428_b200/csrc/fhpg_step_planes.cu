@@ -8,13 +8,15 @@
 // collide_rows with its counter-RNG chirality and forcing (step.cpp:63-93),
 // bit-exactly.
 //
-// Layout. A lattice row keeps its W bytes but holds 8 bit planes of W/8 bytes:
-// plane p (0-5 movers NW..W, 6 rest, 7 obstacle), bit j of word i = column
-// 32 i + j. Row pitch, halo rows and spare rows are those of the byte layout,
-// so halo exchange, row strips and buffer sizes do not change. The obstacle
-// plane is static: it is written into both ping-pong buffers by the pack
-// kernel and never by the step, so a step moves exactly the algorithmic
-// 15 bits per site (8 planes read, 7 written).
+// Layout. A lattice row holds 8 bit planes (0-5 movers NW..W, 6 rest, 7
+// obstacle); bit j of word i of a plane = column 32 i + j. Each plane row is
+// W/32 words plus 4 pad words on either side holding the periodic wrap
+// (words W/32-4 .. W/32-1 on the left, 0 .. 3 on the right), so a row is
+// W + 256 bytes and every band's row, edges included, is one rectangular
+// TMA box. Pitch, halo rows and spare rows follow the byte layout. The
+// obstacle plane is static: the pack kernel writes it into both ping-pong
+// buffers and the step never does, so a step moves the algorithmic 15 bits
+// per site (8 planes read, 7 written) plus the pad words.
 //
 // Work decomposition. A warp owns a band of 32 * NW words (1024 NW columns)
 // and a segment of rows that it streams top to bottom; lane l holds words
@@ -34,6 +36,9 @@
 // post-collision candidates (fluid, W set, E clear).
 #include <cstdint>
 #include <type_traits>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "fhpg_common.cuh"
 #include "fhpg_kernels.cuh"
@@ -104,11 +109,13 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "=r"(done) : "r"(bar), "r"(parity) : "memory");
   } while (!done);
 }
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t bar) {
+// One TMA box {72 words, 8 planes, 1 row} of the plane tensor.
+__device__ __forceinline__ void tma_row(uint32_t dst, const CUtensorMap* map, int word, int row,
+                                        uint32_t bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(map), "r"(word), "r"(0), "r"(row), "r"(bar) : "memory");
 }
 
 template <int NW>
@@ -121,8 +128,8 @@ __device__ __forceinline__ void stv(uint32_t* p, const uint32_t (&v)[NW]) {
 }
 
 // Geometry of a warp's smem: a ring of kSlots source rows. A slot holds the
-// 8 planes of the band, each as [16 B left edge chunk | band words | 16 B
-// right edge chunk] so that the +-1 column funnel shifts read the
+// 8 planes of the band, each as [4 words left of the band | band words | 4
+// words right of it] (one TMA box), so the +-1 column funnel shifts read the
 // neighbouring lane's (or band's) word straight from shared memory.
 template <int NW, bool FORCE>
 struct Geo {
@@ -134,44 +141,17 @@ struct Geo {
   static constexpr int kList = 16 * kBandWords;   // walk list entries (uint4)
   static constexpr int kOut = 4 * kBandWords;     // walk result words
   static constexpr int kWarp = (kSlots * kSlot + kList + kOut + 8 * kSlots + 127) / 128 * 128;
-  static constexpr uint32_t kRowBytes = 8u * 4u * kBandWords + 4u * 16u;
+  static constexpr uint32_t kRowBytes = kSlot;
 };
 
 struct Lanes {
   int lane;
   int WW;           // words per plane row (W / 32)
+  int PW;           // words per padded plane row (W / 32 + 8)
   int w0;           // first word of the band
-  int wl, wr;       // first word of the left / right edge chunks (periodic)
+  int pad;          // this lane's words also go to the pad at this word offset (0: none)
+  bool pad_band;    // warp-uniform: some lane of the band writes a pad
 };
-
-// Planes that shift for a source row of global parity PS (pull offsets,
-// backends.cpp:64-73, with the destination row's parity q):
-//   PS = 0: plane 0 R (dest s-1, q=1), 2 L, 4 R (dest s+1, q=1), 5 R
-//   PS = 1: plane 1 L (dest s-1, q=0), 2 L, 3 L (dest s+1, q=0), 5 R
-// Issue the bulk copies of source row `row` (local index) into `slot`
-// (called by one lane).
-template <int NW, bool FORCE>
-__device__ __forceinline__ void issue_row(const uint8_t* src, long long pitch, long long row,
-                                          int ps, const Lanes& L, uint32_t slot, uint32_t bar) {
-  using G = Geo<NW, FORCE>;
-  const uint8_t* r = src + row * pitch;
-  const size_t pb = static_cast<size_t>(L.WW) * 4;  // bytes per plane row
-  mbar_expect_tx(bar, G::kRowBytes);
-#pragma unroll
-  for (int p = 0; p < 8; ++p)
-    bulk_g2s(slot + p * G::kPlane + 16, r + p * pb + L.w0 * 4, 4 * G::kBandWords, bar);
-  const int pl0 = ps ? 1 : 0, pl3 = ps ? 3 : 4;
-  // left chunks for L shifts, right chunks for R shifts
-  if (ps) {
-    bulk_g2s(slot + pl0 * G::kPlane, r + pl0 * pb + L.wl * 4, 16, bar);
-    bulk_g2s(slot + pl3 * G::kPlane, r + pl3 * pb + L.wl * 4, 16, bar);
-  } else {
-    bulk_g2s(slot + pl0 * G::kPlane + 16 + 4 * G::kBandWords, r + pl0 * pb + L.wr * 4, 16, bar);
-    bulk_g2s(slot + pl3 * G::kPlane + 16 + 4 * G::kBandWords, r + pl3 * pb + L.wr * 4, 16, bar);
-  }
-  bulk_g2s(slot + 2 * G::kPlane, r + 2 * pb + L.wl * 4, 16, bar);
-  bulk_g2s(slot + 5 * G::kPlane + 16 + 4 * G::kBandWords, r + 5 * pb + L.wr * 4, 16, bar);
-}
 
 // Plane words of this lane from a slot: aligned, or shifted by one column.
 template <int NW>
@@ -207,15 +187,16 @@ __device__ __forceinline__ void rd_shr(uint32_t a, uint32_t (&o)[NW]) {
 
 // Balanced walk over the set bits of the warp's NW * 32 mask words (word
 // i = lane * NW + w <-> band word i, bit j <-> column 32 i + j of the band).
-// The warp's nonzero words go to a list {mask, word, sites before it}; the
-// T sites are split into 32 equal contiguous slices; each lane finds its
-// first word (binary search over the lanes' counts), skips the sites before
-// its slice and visits its sites two at a time, advancing through the list
-// (no empty words on it). fn(col0, col1, has1) returns the two result bits,
-// ORed into the result words (osm) bit by bit. Returns T.
+// The warp's nonzero words go to a list {mask, key address of the word's
+// first column, sites before it, result word address}; the T sites are
+// split into 32 equal contiguous slices; each lane finds its first word
+// (binary search over the lanes' counts), skips the sites before its slice
+// and visits its sites two at a time, advancing through the list (it has
+// no empty words). fn(key address) returns the site's result bit, ORed into
+// the result words (osm). Returns T.
 template <int NW, typename Fn>
-__device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint32_t osm, int lane,
-                                    Fn&& fn) {
+__device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint32_t osm,
+                                    uint32_t keys, int lane, Fn&& fn) {
   int cnt = 0, nz = 0;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
@@ -237,7 +218,8 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
 #pragma unroll
     for (int w = 0; w < NW; ++w) {
       if (m[w]) {
-        sts128(lsm + q * 16, m[w], static_cast<uint32_t>(lane * NW + w), static_cast<uint32_t>(c), 0u);
+        const uint32_t wi = static_cast<uint32_t>(lane * NW + w);
+        sts128(lsm + q * 16, m[w], keys + wi * 256u, static_cast<uint32_t>(c), osm + wi * 4u);
         ++q;
         c += __popc(m[w]);
       }
@@ -263,29 +245,36 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
       ++q;
       en = lds128(lsm + q * 16);
     }
-    uint32_t mask = en.x;
-    uint32_t base = en.y * 32u;
+    uint32_t mask = en.x, kw = en.y, ow = en.w;
     for (int k = s - static_cast<int>(en.z); k > 0; --k) mask ^= 1u << top_bit(mask);
-    auto next = [&](uint32_t& col) {
+    // site: key address, result word address, bit
+    auto next = [&](uint32_t& ka, uint32_t& wa, uint32_t& bit) {
       if (mask == 0u) {
         ++q;
         const uint4 n = lds128(lsm + q * 16);
         mask = n.x;
-        base = n.y * 32u;
+        kw = n.y;
+        ow = n.w;
       }
       const uint32_t j = top_bit(mask);
-      mask ^= 1u << j;
-      col = base + j;
+      bit = 1u << j;
+      mask ^= bit;
+      ka = kw + j * 8u;
+      wa = ow;
     };
-    for (int it = s; it < e; it += 2) {
-      uint32_t c0, c1 = 0;
-      next(c0);
-      const bool has1 = it + 1 < e;
-      if (has1) next(c1);
-      uint32_t b0, b1;
-      fn(c0, c1, has1, b0, b1);
-      red_or(osm + (c0 >> 5) * 4u, b0 << (c0 & 31u));
-      red_or(osm + (c1 >> 5) * 4u, b1 << (c1 & 31u));
+    int it = s;
+    for (; it + 1 < e; it += 2) {
+      uint32_t k0, w0, m0, k1, w1, m1;
+      next(k0, w0, m0);
+      next(k1, w1, m1);
+      const uint32_t b0 = fn(k0), b1 = fn(k1);
+      red_or(w0, b0 ? m0 : 0u);
+      red_or(w1, b1 ? m1 : 0u);
+    }
+    if (it < e) {
+      uint32_t k0, w0, m0;
+      next(k0, w0, m0);
+      if (fn(k0)) red_or(w0, m0);
     }
   }
   __syncwarp();
@@ -306,7 +295,8 @@ struct Ctx {
 template <int NW, bool FORCE, int Q>
 __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
                                          const Ctx<NW, FORCE>& cx, int lane, uint32_t y,
-                                         uint32_t* out_row, int plane_words, unsigned& swaps) {
+                                         uint32_t* out_row, int plane_words, int pad,
+                                         bool pad_band, unsigned& swaps) {
   using G = Geo<NW, FORCE>;
   constexpr int P = G::kPlane;
   uint32_t a0[NW], a1[NW], a2[NW], a3[NW], a4[NW], a5[NW], rr[NW], so[NW];
@@ -330,13 +320,8 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   }
   // Chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y)
   // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76).
-  const int T = walk<NW>(dep, cx.lsm, cx.osm, lane,
-                         [&](uint32_t c0, uint32_t c1, bool has1, uint32_t& b0, uint32_t& b1) {
-    const uint64_t k0 = lds64(cx.kc + c0 * 8u);
-    const uint64_t k1 = lds64(cx.kc + c1 * 8u);
-    b0 = fin64_bit0(k0 + y);
-    b1 = fin64_bit0(k1 + y) & (has1 ? 1u : 0u);
-  });
+  const int T = walk<NW>(dep, cx.lsm, cx.osm, cx.kc, lane,
+                         [&](uint32_t ka) { return fin64_bit0(lds64(ka) + y); });
   uint32_t o[NW][7];
   const uint32_t mine = cx.osm + lane * NW * 4;
 #pragma unroll
@@ -353,12 +338,8 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
     uint32_t f[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) f[w] = ~so[w] & o[w][5] & ~o[w][2];
-    const int TF = walk<NW>(f, cx.lsm, cx.osm, lane,
-                            [&](uint32_t c0, uint32_t c1, bool has1, uint32_t& b0, uint32_t& b1) {
-      const uint64_t k0 = lds64(cx.kf + c0 * 8u);
-      const uint64_t k1 = lds64(cx.kf + c1 * 8u);
-      b0 = (fin64(k0 + y) >> 32) < cx.thr ? 1u : 0u;
-      b1 = has1 && (fin64(k1 + y) >> 32) < cx.thr ? 1u : 0u;
+    const int TF = walk<NW>(f, cx.lsm, cx.osm, cx.kf, lane, [&](uint32_t ka) {
+      return (fin64(lds64(ka) + y) >> 32) < cx.thr ? 1u : 0u;
     });
     if (TF) {
 #pragma unroll
@@ -376,51 +357,60 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
 #pragma unroll
     for (int w = 0; w < NW; ++w) v[w] = o[w][p];
     stv<NW>(out_row + p * plane_words, v);
+    if (pad_band && pad != 0) stv<NW>(out_row + p * plane_words + pad, v);  // periodic wrap copy
   }
 }
 
 template <int NW, bool FORCE, int Q0>
-__device__ __forceinline__ void run_segment(const StepArgs& a, const Lanes& L, uint32_t ring,
-                                            uint32_t bars, const Ctx<NW, FORCE>& cx, int r_begin,
-                                            int r_end, unsigned& swaps) {
+__device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap* map,
+                                            const Lanes& L, uint32_t ring, uint32_t bars,
+                                            const Ctx<NW, FORCE>& cx, int r_begin, int r_end,
+                                            unsigned& swaps) {
   using G = Geo<NW, FORCE>;
   const long long pitch = static_cast<long long>(a.pitch);
-  const int first = r_begin - 1;          // source rows first .. r_end
+  const int first = r_begin - 1;  // source rows first .. r_end (local; tensor row = local + 1)
   const int last = r_end;
   const uint32_t lane_off = 16u + L.lane * NW * 4u;
-  auto slot_of = [&](int row) { return static_cast<uint32_t>((row - first) % G::kSlots); };
-  auto issue = [&](int row) {
+  // Ring position of the next row to issue / of rows r-1, r, r+1, and the
+  // mbarrier phase of each slot, tracked incrementally.
+  uint32_t phase = 0;  // bit k: phase of slot k's next completion
+  int issue_row = first, issue_slot = 0;
+  auto issue = [&]() {
     if (L.lane == 0) {
-      const uint32_t k = slot_of(row);
-      issue_row<NW, FORCE>(a.src, pitch, row, static_cast<int>((a.row0 + row) & 1), L,
-                           ring + k * G::kSlot, bars + k * 8u);
+      const uint32_t bar = bars + issue_slot * 8u;
+      mbar_expect_tx(bar, G::kRowBytes);
+      tma_row(ring + issue_slot * G::kSlot, map, L.w0, issue_row + 1, bar);
     }
+    ++issue_row;
+    issue_slot = issue_slot + 1 == G::kSlots ? 0 : issue_slot + 1;
   };
-  auto wait = [&](int row) {
-    const uint32_t k = slot_of(row);
-    mbar_wait(bars + k * 8u, static_cast<uint32_t>(((row - first) / G::kSlots) & 1));
+  auto wait = [&](int slot) {
+    mbar_wait(bars + slot * 8u, (phase >> slot) & 1u);
+    phase ^= 1u << slot;
   };
-  const int pro = min(last, first + G::kSlots - 1);
-  for (int row = first; row <= pro; ++row) issue(row);
-  wait(first);
-  wait(first + 1);
+  while (issue_row <= last && issue_row < first + G::kSlots) issue();
+  int sm = 0, sc = 1, sn = 2;  // slots of rows r-1, r, r+1
+  wait(sm);
+  wait(sc);
   const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
-  uint32_t* out = reinterpret_cast<uint32_t*>(a.dst + r_begin * pitch) + L.w0 + L.lane * NW;
+  uint32_t* out = reinterpret_cast<uint32_t*>(a.dst + r_begin * pitch) + 4 + L.w0 + L.lane * NW;
   const long long pw = pitch / 4;
   auto one = [&](int r, auto qc) {
     constexpr int Q = decltype(qc)::value;
-    wait(r + 1);
-    dest_row<NW, FORCE, Q>(ring + slot_of(r - 1) * G::kSlot + lane_off,
-                           ring + slot_of(r) * G::kSlot + lane_off,
-                           ring + slot_of(r + 1) * G::kSlot + lane_off, cx, L.lane, y0 + r, out,
-                           L.WW, swaps);
+    wait(sn);
+    dest_row<NW, FORCE, Q>(ring + sm * G::kSlot + lane_off, ring + sc * G::kSlot + lane_off,
+                           ring + sn * G::kSlot + lane_off, cx, L.lane, y0 + r, out, L.PW, L.pad,
+                           L.pad_band, swaps);
     out += pw;
-    // Slot of row r-1 is free once every lane has read it.
+    // The slot of row r-1 is free once every lane has read it.
     __syncwarp();
-    if (r - 1 + G::kSlots <= last) {
+    if (issue_row <= last) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(r - 1 + G::kSlots);
+      issue();
     }
+    sm = sc;
+    sc = sn;
+    sn = sn + 1 == G::kSlots ? 0 : sn + 1;
   };
   int r = r_begin;
   for (; r + 2 <= r_end; r += 2) {
@@ -431,7 +421,8 @@ __device__ __forceinline__ void run_segment(const StepArgs& a, const Lanes& L, u
 }
 
 template <int NW, bool FORCE>
-__global__ void __launch_bounds__(kPThreads, 1) step_planes_kernel(StepArgs a) {
+__global__ void __launch_bounds__(kPThreads, 1)
+    step_planes_kernel(StepArgs a, const __grid_constant__ CUtensorMap map) {
   using G = Geo<NW, FORCE>;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
@@ -477,9 +468,12 @@ __global__ void __launch_bounds__(kPThreads, 1) step_planes_kernel(StepArgs a) {
   Lanes L;
   L.lane = threadIdx.x & 31;
   L.WW = a.W >> 5;
+  L.PW = L.WW + 8;
   L.w0 = band * G::kBandWords;
-  L.wl = L.w0 == 0 ? L.WW - 4 : L.w0 - 4;
-  L.wr = L.w0 + G::kBandWords == L.WW ? 0 : L.w0 + G::kBandWords;
+  // Lanes holding words 0..3 / WW-4..WW-1 also write the right / left pad.
+  const int wl = L.w0 + L.lane * NW;
+  L.pad = wl < 4 ? L.WW : (wl >= L.WW - 4 ? -L.WW : 0);
+  L.pad_band = L.w0 == 0 || L.w0 + G::kBandWords == L.WW;
   Ctx<NW, FORCE> cx;
   cx.kc = kc_base + bic * G::kBandCols * 8;
   cx.kf = kf_base + bic * G::kBandCols * 8;
@@ -488,9 +482,9 @@ __global__ void __launch_bounds__(kPThreads, 1) step_planes_kernel(StepArgs a) {
   cx.thr = a.thr;
   unsigned swaps = 0;
   if ((a.row0 + r_begin) & 1)
-    run_segment<NW, FORCE, 1>(a, L, ring, bars, cx, r_begin, r_end, swaps);
+    run_segment<NW, FORCE, 1>(a, &map, L, ring, bars, cx, r_begin, r_end, swaps);
   else
-    run_segment<NW, FORCE, 0>(a, L, ring, bars, cx, r_begin, r_end, swaps);
+    run_segment<NW, FORCE, 0>(a, &map, L, ring, bars, cx, r_begin, r_end, swaps);
   if (FORCE) {
     unsigned long long s = swaps;
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
@@ -505,7 +499,7 @@ int smem_bytes(int bpc) {
 }
 
 template <int NW, bool FORCE>
-void launch_nw(StepArgs a, int num_sms, cudaStream_t st) {
+void launch_nw(StepArgs a, const CUtensorMap& map, int num_sms, cudaStream_t st) {
   using G = Geo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
   a.nbands = a.W / G::kBandCols;
@@ -532,7 +526,7 @@ void launch_nw(StepArgs a, int num_sms, cudaStream_t st) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  step_planes_kernel<NW, FORCE><<<grid, kPThreads, smem, st>>>(a);
+  step_planes_kernel<NW, FORCE><<<grid, kPThreads, smem, st>>>(a, map);
 }
 
 // ---------------------------------------------------------------------------
@@ -563,16 +557,22 @@ __global__ void pack_kernel(const uint8_t* src, const uint8_t* mask, uint8_t* ds
       const uint32_t nz1 = (nz2 | (nz2 >> 1)) & 0x01010101u;
       v[k] = (v[k] & 0x7F7F7F7Fu) | (nz1 << 7);
     }
-    uint32_t* d = reinterpret_cast<uint32_t*>(dst + r * static_cast<long long>(pitch)) + i;
+    const int PW = WW + 8;  // padded plane row
+    const int pad = i < 4 ? WW : (i >= WW - 4 ? -WW : 0);
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst + r * static_cast<long long>(pitch)) + 4 + i;
+    uint32_t* o = reinterpret_cast<uint32_t*>(dst_obst + r * static_cast<long long>(pitch)) + 4 + i;
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       uint32_t w = 0;
 #pragma unroll
       for (int k = 0; k < 8; ++k)  // bytes 4k..4k+3: bit p of each -> 4 bits
         w |= ((((v[k] >> p) & 0x01010101u) * 0x01020408u) >> 24 & 0xFu) << (4 * k);
-      d[p * WW] = w;
-      if (p == 7)
-        reinterpret_cast<uint32_t*>(dst_obst + r * static_cast<long long>(pitch))[7 * WW + i] = w;
+      d[p * PW] = w;
+      if (pad) d[p * PW + pad] = w;
+      if (p == 7) {
+        o[7 * PW] = w;
+        if (pad) o[7 * PW + pad] = w;
+      }
     }
   }
 }
@@ -584,10 +584,11 @@ __global__ void unpack_kernel(const uint8_t* src, uint8_t* dst, size_t pitch, in
        t += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long r = t / WW;
     const int i = static_cast<int>(t % WW);
-    const uint32_t* s = reinterpret_cast<const uint32_t*>(src + r * static_cast<long long>(pitch)) + i;
+    const uint32_t* s =
+        reinterpret_cast<const uint32_t*>(src + r * static_cast<long long>(pitch)) + 4 + i;
     uint32_t p[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) p[q] = s[q * WW];
+    for (int q = 0; q < 8; ++q) p[q] = s[q * (WW + 8)];
     uint32_t v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -618,15 +619,44 @@ int planes_words_per_lane(int W) {
 
 bool planes_ok(int W) { return planes_words_per_lane(W) != 0; }
 
-int launch_step_planes(const StepArgs& a, int num_sms, cudaStream_t st) {
+size_t planes_row_bytes(int W) { return static_cast<size_t>(W) + 256; }
+
+bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+  }
+  // {padded words, planes, rows}; box {72 words, 8 planes, 1 row} (one band
+  // of 64 words + 4 on each side; NW = 1 bands of 32 words use {40, 8, 1}).
+  const int nw = planes_words_per_lane(W);
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(W / 32 + 8), 8,
+                              static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>((W / 32 + 8) * 4),
+                                 static_cast<cuuint64_t>(pitch)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(32 * nw + 8), 8, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(static_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
+                            buffer, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int launch_step_planes(const StepArgs& a, const void* tmap_src, int num_sms, cudaStream_t st) {
   const int nw = planes_words_per_lane(a.W);
   const bool force = a.thr != 0;
+  const CUtensorMap& m = *static_cast<const CUtensorMap*>(tmap_src);
   if (nw == 2) {
-    if (force) launch_nw<2, true>(a, num_sms, st);
-    else launch_nw<2, false>(a, num_sms, st);
+    if (force) launch_nw<2, true>(a, m, num_sms, st);
+    else launch_nw<2, false>(a, m, num_sms, st);
   } else {
-    if (force) launch_nw<1, true>(a, num_sms, st);
-    else launch_nw<1, false>(a, num_sms, st);
+    if (force) launch_nw<1, true>(a, m, num_sms, st);
+    else launch_nw<1, false>(a, m, num_sms, st);
   }
   return 1;
 }
