@@ -34,80 +34,123 @@
 
 namespace fhpg {
 
-// FHP-III, phase 1 output.
+// Three-input boolean function as one LOP3; LUT = f(0xF0, 0xCC, 0xAA) & 0xFF.
+constexpr uint32_t kLA = 0xF0, kLB = 0xCC, kLC = 0xAA;
+#define FHPG_LUT(expr) ((expr) & 0xFFu)
+template <uint32_t LUT>
+FHPG_HD uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return d;
+#else
+  uint32_t d = 0;
+  for (int m = 0; m < 8; ++m)
+    if ((LUT >> m) & 1u) d |= ((m & 4) ? a : ~a) & ((m & 2) ? b : ~b) & ((m & 1) ? c : ~c);
+  return d;
+#endif
+}
+constexpr uint32_t kMaj = FHPG_LUT((kLA & kLB) | (kLA & kLC) | (kLB & kLC));
+constexpr uint32_t kXor3 = FHPG_LUT(kLA ^ kLB ^ kLC);
+constexpr uint32_t kOr3 = FHPG_LUT(kLA | kLB | kLC);
+constexpr uint32_t kNor3 = FHPG_LUT(~(kLA | kLB | kLC));
+constexpr uint32_t kAndOr = FHPG_LUT((kLA & kLB) | kLC);          // (a & b) | c
+constexpr uint32_t kMux = FHPG_LUT((kLA & kLB) | (~kLA & kLC));   // a ? b : c
+// Reduced pair / reduced a_i & a_j: c ? ~(a | b) : a & b (c = D).
+constexpr uint32_t kRedAnd = FHPG_LUT((kLC & ~(kLA | kLB)) | (~kLC & kLA & kLB));
+// Reduced single: c ? ~a & b : a & ~b.
+constexpr uint32_t kRedSingle = FHPG_LUT((kLC & ~kLA & kLB) | (~kLC & kLA & ~kLB));
+
+// FHP-III, phase 1 output: class masks kept across the chirality walk.
 struct Fhp3Class {
-  uint32_t ap[6];  // movers after the particle-hole reduction
-  uint32_t rp;     // rest after the reduction
   uint32_t D;      // sites with mass >= 4 (complemented)
-  uint32_t ROT, BB, X, B, AY, KEEP, xp;
+  uint32_t ROT, BB, X, B, AY, Y, KEEP, xp;
   uint32_t dep;
 };
 
-FHPG_HD uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (a & c) | (b & c); }
-
-FHPG_HD Fhp3Class fhp3_classify(const uint32_t a[6], uint32_t r, uint32_t solid) {
+FHPG_HD Fhp3Class fhp3_classify(const uint32_t a[6], uint32_t r, uint32_t s) {
   Fhp3Class k;
   // mass >= 4 of the 7 bits: carries of three full adders, then a majority.
-  const uint32_t c1 = maj3(a[0], a[1], a[2]), c2 = maj3(a[3], a[4], a[5]);
-  const uint32_t s1 = a[0] ^ a[1] ^ a[2], s2 = a[3] ^ a[4] ^ a[5];
-  const uint32_t c3 = maj3(s1, s2, r);
-  const uint32_t D = maj3(c1, c2, c3);
+  const uint32_t c1 = lop3<kMaj>(a[0], a[1], a[2]), c2 = lop3<kMaj>(a[3], a[4], a[5]);
+  const uint32_t s1 = lop3<kXor3>(a[0], a[1], a[2]), s2 = lop3<kXor3>(a[3], a[4], a[5]);
+  const uint32_t c3 = lop3<kMaj>(s1, s2, r);
+  const uint32_t D = lop3<kMaj>(c1, c2, c3);
   k.D = D;
-#pragma unroll
-  for (int i = 0; i < 6; ++i) k.ap[i] = a[i] ^ D;
-  k.rp = r ^ D;
-  const uint32_t fl = ~solid;
-  // Axis signals (O is unchanged by the reduction).
+  const uint32_t rp = r ^ D;
+  // Axis signals: O (odd axis) is unchanged by the reduction; a pair of the
+  // reduced state is a pair (D = 0) or an empty axis (D = 1) of the original.
   const uint32_t O0 = a[0] ^ a[3], O1 = a[1] ^ a[4], O2 = a[2] ^ a[5];
-  const uint32_t P0 = k.ap[0] & k.ap[3], P1 = k.ap[1] & k.ap[4], P2 = k.ap[2] & k.ap[5];
-  const uint32_t anyP = P0 | P1 | P2;
-  const uint32_t no0 = ~(O0 | O1 | O2);
-  const uint32_t ex1 = (O0 ^ O1 ^ O2) & ~(O0 & O1 & O2);
-  const uint32_t ex2 = maj3(O0, O1, O2) & ~(O0 & O1 & O2);
-  const uint32_t O3 = O0 & O1 & O2;
-  // Three odd axes (3 movers, no rest): a symmetric triple iff a0 == a2 == a4.
-  const uint32_t eqv = ~((k.ap[0] ^ k.ap[2]) | (k.ap[2] ^ k.ap[4]));
-  k.BB = solid | (O3 & eqv);
-  k.ROT = no0 & fl;
-  k.X = ex1 & anyP & fl;
-  k.B = ex1 & ~anyP & k.rp & fl;
-  // Two odd axes, movers 120 deg apart <=> both on the same sublattice.
-  const uint32_t ev = k.ap[0] | k.ap[2] | k.ap[4], od = k.ap[1] | k.ap[3] | k.ap[5];
-  k.AY = ex2 & (ev ^ od) & fl;
-  k.KEEP = fl & ~(k.ROT | k.BB | k.X | k.B | k.AY);
+  const uint32_t P0 = lop3<kRedAnd>(a[0], a[3], D);
+  const uint32_t P1 = lop3<kRedAnd>(a[1], a[4], D);
+  const uint32_t P2 = lop3<kRedAnd>(a[2], a[5], D);
+  const uint32_t anyP = lop3<kOr3>(P0, P1, P2);
+  k.ROT = lop3<kNor3>(O0, O1, O2) & ~s;
+  const uint32_t ex1 = lop3<FHPG_LUT((kLA ^ kLB ^ kLC) & ~(kLA & kLB & kLC))>(O0, O1, O2);
+  const uint32_t ex2 = lop3<FHPG_LUT(((kLA & kLB) | (kLA & kLC) | (kLB & kLC)) & ~(kLA & kLB & kLC))>(O0, O1, O2);
+  const uint32_t O3 = lop3<FHPG_LUT(kLA & kLB & kLC)>(O0, O1, O2);
+  // Three odd axes (3 movers, no rest): a symmetric triple iff a0 == a2 == a4
+  // (invariant under the reduction). Obstacles bounce back too.
+  const uint32_t eqv = lop3<FHPG_LUT((kLA & kLB & kLC) | (~kLA & ~kLB & ~kLC))>(a[0], a[2], a[4]);
+  k.BB = lop3<FHPG_LUT(kLA | (kLB & kLC))>(s, O3, eqv);
+  const uint32_t exf1 = ex1 & ~s;
+  k.X = exf1 & anyP;
+  k.B = lop3<FHPG_LUT(kLA & ~kLB & kLC)>(exf1, anyP, rp);
+  // Two odd axes with movers 120 deg apart <=> both on directions of the
+  // same parity <=> an even number of odd-direction singles (invariant).
+  const uint32_t v1 = a[1] & ~a[4], v3 = a[3] & ~a[0], v5 = a[5] & ~a[2];
+  const uint32_t pi = lop3<kXor3>(v1, v3, v5);
+  k.AY = lop3<FHPG_LUT(kLA & ~kLB & ~kLC)>(ex2, pi, s);
+  k.Y = k.AY & rp;
+  const uint32_t t = lop3<kOr3>(k.ROT, k.X, k.B);
+  k.KEEP = lop3<kNor3>(t, k.BB, k.AY);
   // X states: the pair's axis follows the odd axis (X+) or precedes it (X-).
-  k.xp = (O0 & P1) | (O1 & P2) | (O2 & P0);
-  k.dep = (k.ROT & anyP) | k.X | (k.AY & k.rp);
+  const uint32_t x1 = O0 & P1;
+  const uint32_t x2 = lop3<kAndOr>(O1, P2, x1);
+  k.xp = lop3<kAndOr>(O2, P0, x2);
+  const uint32_t d1 = lop3<kAndOr>(k.ROT, anyP, k.X);
+  k.dep = d1 | k.Y;
   return k;
 }
 
-FHPG_HD void fhp3_apply(const Fhp3Class& k, uint32_t c, uint32_t r, uint32_t o[6],
-                        uint32_t& o_r) {
-  const uint32_t* a = k.ap;
+// a: the original movers (as passed to fhp3_classify), r: the original rest.
+FHPG_HD void fhp3_apply(const Fhp3Class& k, uint32_t c, uint32_t r, const uint32_t a[6],
+                        uint32_t o[6], uint32_t& o_r) {
   // X -> Y for X+ with c = 1 and X- with c = 0; otherwise the pair moves.
-  const uint32_t toY = ~(k.xp ^ c);
-  const uint32_t NX = k.X & ~toY;
-  const uint32_t U = (k.X & toY) | k.B;
-  const uint32_t BNX = k.BB | NX;
-  uint32_t rot[6], v[6];
+  const uint32_t NX = lop3<FHPG_LUT(kLA & (kLB ^ kLC))>(k.X, k.xp, c);
+  const uint32_t U = lop3<FHPG_LUT((kLA & ~kLB) | kLC)>(k.X, NX, k.B);
+  const uint32_t UAY = U | k.AY;
+  // Permutation classes act on the original movers (the reduction cancels):
+  // rotation (c ? a_{k-1} : a_{k+1}), bounce-back / pair move (a_{k+3}, NX
+  // complemented by DN), keep (a_k). U / AY classes use reduced movers and
+  // are complemented back with D.
+  const uint32_t S3 = k.BB | NX;
+  const uint32_t DN = lop3<FHPG_LUT(kLA | (kLB & kLC))>(NX, k.D, UAY);
+  uint32_t v[6], g[6];
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
-    rot[i] = (c & a[(i + 5) % 6]) | (~c & a[(i + 1) % 6]);
-    v[i] = a[i] & ~a[(i + 3) % 6];
+    v[i] = lop3<kRedSingle>(a[i], a[(i + 3) % 6], k.D);  // reduced: odd mover of its axis
+    g[i] = lop3<kRedAnd>(a[i], a[(i + 4) % 6], k.D);     // reduced: a_i & a_{i-2}
   }
+  // Y -> X: the pair lands on the axis of the mover whose partner sits at
+  // -120 deg (c = 0) or +120 deg (c = 1).
+  uint32_t GY[3], PA[3];
+#pragma unroll
+  for (int m = 0; m < 3; ++m) GY[m] = lop3<FHPG_LUT(kLA & (kLB | kLC))>(k.Y, g[m], g[m + 3]);
+#pragma unroll
+  for (int m = 0; m < 3; ++m) PA[m] = lop3<kMux>(c, GY[(m + 2) % 3], GY[m]);
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
-    const uint32_t am = a[(i + 5) % 6], apl = a[(i + 1) % 6], opp = a[(i + 3) % 6];
-    const uint32_t t = am & apl;
-    const uint32_t pp = (a[i] & rot[(i + 3) % 6]) | (opp & rot[i]);
-    const uint32_t ay = t | (k.rp & pp);
-    const uint32_t u = v[(i + 5) % 6] | v[(i + 1) % 6];
-    const uint32_t acc = (k.ROT & rot[i]) | (BNX & (opp ^ NX)) | (U & u) | (k.AY & ay) |
-                         (k.KEEP & a[i]);
-    o[i] = acc ^ k.D;
+    const uint32_t rot = lop3<kMux>(c, a[(i + 5) % 6], a[(i + 1) % 6]);
+    uint32_t acc = lop3<kAndOr>(k.ROT, rot, S3 & a[(i + 3) % 6]);
+    acc = lop3<kAndOr>(k.KEEP, a[i], acc);
+    // B -> A, X -> Y: v_{i-1} | v_{i+1}; A -> B (and Y's single): v_{i-1} & v_{i+1}
+    const uint32_t q = lop3<FHPG_LUT((kLC & kLA & kLB) | (~kLC & (kLA | kLB)))>(
+        v[(i + 5) % 6], v[(i + 1) % 6], k.AY);
+    acc = lop3<kAndOr>(UAY, q, acc);
+    o[i] = lop3<FHPG_LUT((kLA | kLB) ^ kLC)>(acc, PA[i % 3], DN);
   }
   // The rest flips exactly for B -> A, X -> Y, A -> B, Y -> X (unchanged by D).
-  o_r = r ^ (U | k.AY);
+  o_r = lop3<FHPG_LUT(kLA ^ (kLB | kLC))>(r, U, k.AY);
 }
 
 }  // namespace fhpg

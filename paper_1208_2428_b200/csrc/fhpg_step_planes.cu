@@ -239,42 +239,41 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
   }
   const int o_excl = __shfl_sync(kFull, excl, o);
   if (s < e) {
-    int q = o_excl >> 16;
-    uint4 en = lds128(lsm + q * 16);
+    uint32_t qa = lsm + (o_excl >> 16) * 16u;  // list entry address
+    uint4 en = lds128(qa);
     if (NW > 1 && s >= static_cast<int>(en.z) + __popc(en.x)) {
-      ++q;
-      en = lds128(lsm + q * 16);
+      qa += 16u;
+      en = lds128(qa);
     }
     uint32_t mask = en.x, kw = en.y, ow = en.w;
     for (int k = s - static_cast<int>(en.z); k > 0; --k) mask ^= 1u << top_bit(mask);
-    // site: key address, result word address, bit
-    auto next = [&](uint32_t& ka, uint32_t& wa, uint32_t& bit) {
+    // site: key address, result word address, bit index
+    auto next = [&](uint32_t& ka, uint32_t& wa, uint32_t& j) {
       if (mask == 0u) {
-        ++q;
-        const uint4 n = lds128(lsm + q * 16);
+        qa += 16u;
+        const uint4 n = lds128(qa);
         mask = n.x;
         kw = n.y;
         ow = n.w;
       }
-      const uint32_t j = top_bit(mask);
-      bit = 1u << j;
-      mask ^= bit;
+      j = top_bit(mask);
+      mask ^= 1u << j;
       ka = kw + j * 8u;
       wa = ow;
     };
     int it = s;
     for (; it + 1 < e; it += 2) {
-      uint32_t k0, w0, m0, k1, w1, m1;
-      next(k0, w0, m0);
-      next(k1, w1, m1);
+      uint32_t k0, w0, j0, k1, w1, j1;
+      next(k0, w0, j0);
+      next(k1, w1, j1);
       const uint32_t b0 = fn(k0), b1 = fn(k1);
-      red_or(w0, b0 ? m0 : 0u);
-      red_or(w1, b1 ? m1 : 0u);
+      red_or(w0, b0 << j0);
+      red_or(w1, b1 << j1);
     }
     if (it < e) {
-      uint32_t k0, w0, m0;
-      next(k0, w0, m0);
-      if (fn(k0)) red_or(w0, m0);
+      uint32_t k0, w0, j0;
+      next(k0, w0, j0);
+      red_or(w0, fn(k0) << j0);
     }
   }
   __syncwarp();
@@ -328,7 +327,8 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   for (int w = 0; w < NW; ++w) {
     const uint32_t c = T ? lds32(mine + w * 4) : 0u;
     uint32_t oo[6], orr;
-    fhp3_apply(K[w], c, rr[w], oo, orr);
+    const uint32_t a[6] = {a0[w], a1[w], a2[w], a3[w], a4[w], a5[w]};
+    fhp3_apply(K[w], c, rr[w], a, oo, orr);
 #pragma unroll
     for (int p = 0; p < 6; ++p) o[w][p] = oo[p];
     o[w][6] = orr;

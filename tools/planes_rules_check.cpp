@@ -39,8 +39,8 @@ static int check(const char* name, int variant, Classify classify, Apply apply) 
     const Words x = pack(w);
     const auto k = classify(x.a, x.r, x.solid);
     uint32_t o0[6], o1[6], r0, r1;
-    apply(k, 0u, x.r, o0, r0);
-    apply(k, ~0u, x.r, o1, r1);
+    apply(k, 0u, x.r, x.a, o0, r0);
+    apply(k, ~0u, x.r, x.a, o1, r1);
     for (int j = 0; j < 32; ++j) {
       const unsigned s = static_cast<unsigned>(w * 32 + j);
       for (int c = 0; c < 2; ++c) {
@@ -70,8 +70,8 @@ int main() {
   int bad = 0;
   bad += check("fhp3", FHPG_RULES_FHP_III,
                [](const uint32_t* a, uint32_t r, uint32_t s) { return fhp3_classify(a, r, s); },
-               [](const Fhp3Class& k, uint32_t c, uint32_t r, uint32_t* o, uint32_t& orr) {
-                 fhp3_apply(k, c, r, o, orr);
+               [](const Fhp3Class& k, uint32_t c, uint32_t r, const uint32_t* x_a, uint32_t* o, uint32_t& orr) {
+                 fhp3_apply(k, c, r, x_a, o, orr);
                });
   return bad ? 1 : 0;
 }
