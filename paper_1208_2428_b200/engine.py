@@ -22,7 +22,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfhpg.so")
+# FHPG_LIB overrides the engine library (A/B builds of kernel variants).
+LIB_PATH = os.environ.get("FHPG_LIB") or os.path.join(_HERE, "lib", "libfhpg.so")
 
 EINVAL = 2
 ERUNTIME = 3
