@@ -44,12 +44,19 @@
 #include "fhpg_kernels.cuh"
 #include "fhpg_planes_rules.cuh"
 
+// 4 words per lane (8 warps per SM) measured slower than 2 (16 warps):
+// 1368 vs 1646 GSUPS on cfg4; build with -DFHPG_PLANES_NW4=4 to select it.
+#ifndef FHPG_PLANES_NW4
+#define FHPG_PLANES_NW4 2
+#endif
+
 namespace fhpg {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kPWarps = 16;
-constexpr int kPThreads = kPWarps * 32;
+// Warps per CTA (one CTA per SM): 16 with 2 words per lane, 8 with 4.
+template <int NW>
+constexpr int kPWarps = NW == 4 ? 8 : 16;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -118,9 +125,41 @@ __device__ __forceinline__ void tma_row(uint32_t dst, const CUtensorMap* map, in
       ::"r"(dst), "l"(map), "r"(word), "r"(0), "r"(row), "r"(bar) : "memory");
 }
 
+// TMA store of a dense smem box (the 7 outgoing planes of a band row, or
+// the 4 pad words of each plane) into the plane tensor; bulk-group tracked.
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, int word, int row, uint32_t src) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
+      ::"l"(map), "r"(word), "r"(0), "r"(row), "r"(src) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+template <int NW>
+__device__ __forceinline__ void stsv(uint32_t a, const uint32_t (&v)[NW]) {
+  if constexpr (NW == 4) {
+    sts128(a, v[0], v[1], v[2], v[3]);
+  } else if constexpr (NW == 2) {
+    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(v[0]), "r"(v[1]));
+  } else {
+    sts32(a, v[0]);
+  }
+}
+
 template <int NW>
 __device__ __forceinline__ void stv(uint32_t* p, const uint32_t (&v)[NW]) {
-  if constexpr (NW == 2) {
+  if constexpr (NW == 4) {
+    __stcs(reinterpret_cast<uint4*>(p), make_uint4(v[0], v[1], v[2], v[3]));
+  } else if constexpr (NW == 2) {
     __stcs(reinterpret_cast<uint2*>(p), make_uint2(v[0], v[1]));
   } else {
     __stcs(p, v[0]);
@@ -137,10 +176,18 @@ struct Geo {
   static constexpr int kBandCols = 1024 * NW;
   static constexpr int kPlane = 32 + 4 * kBandWords;
   static constexpr int kSlot = 8 * kPlane;
-  static constexpr int kSlots = FORCE ? 4 : 5;
-  static constexpr int kList = 16 * kBandWords;   // walk list entries (uint4)
-  static constexpr int kOut = 4 * kBandWords;     // walk result words
-  static constexpr int kWarp = (kSlots * kSlot + kList + kOut + 8 * kSlots + 127) / 128 * 128;
+  static constexpr int kSlots = 4;
+  // Output staging (7 planes x band words, the TMA store source) followed by
+  // the two pad boxes (7 x 4 words each). The walk's list and result words
+  // reuse the staging area: they are dead before the row's outputs land.
+  static constexpr int kStage = 7 * 4 * kBandWords;
+  static constexpr int kPadL = kStage, kPadR = kStage + 128;  // TMA sources: 128 B aligned
+  static constexpr int kList = 16 * kBandWords;   // walk list entries (uint4), inside the stage
+  static constexpr int kOut = 4 * kBandWords;     // walk result words, after the list
+  static_assert(kList + kOut <= kStage + 240, "walk scratch must fit the staging area");
+  static_assert(kStage % 128 == 0, "TMA store sources are 128 B aligned");
+  static constexpr int kStageAll = kStage + 256;
+  static constexpr int kWarp = (kSlots * kSlot + kStageAll + 8 * kSlots + 127) / 128 * 128;
   static constexpr uint32_t kRowBytes = kSlot;
 };
 
@@ -149,14 +196,21 @@ struct Lanes {
   int WW;           // words per plane row (W / 32)
   int PW;           // words per padded plane row (W / 32 + 8)
   int w0;           // first word of the band
-  int pad;          // this lane's words also go to the pad at this word offset (0: none)
+  int pad;          // this lane's words also go to this pad staging offset (-1: none)
+  int padx;         // bit 0: left pad box, bit 1: right pad box (word WW + 4 = (padx >> 2) + 4)
   bool pad_band;    // warp-uniform: some lane of the band writes a pad
 };
 
 // Plane words of this lane from a slot: aligned, or shifted by one column.
 template <int NW>
 __device__ __forceinline__ void rd_al(uint32_t a, uint32_t (&o)[NW]) {
-  if constexpr (NW == 2) {
+  if constexpr (NW == 4) {
+    const uint4 v = lds128(a);
+    o[0] = v.x;
+    o[1] = v.y;
+    o[2] = v.z;
+    o[3] = v.w;
+  } else if constexpr (NW == 2) {
     const uint2 v = lds64v(a);
     o[0] = v.x;
     o[1] = v.y;
@@ -241,9 +295,12 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
   if (s < e) {
     uint32_t qa = lsm + (o_excl >> 16) * 16u;  // list entry address
     uint4 en = lds128(qa);
-    if (NW > 1 && s >= static_cast<int>(en.z) + __popc(en.x)) {
-      qa += 16u;
-      en = lds128(qa);
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      if (s >= static_cast<int>(en.z) + __popc(en.x)) {
+        qa += 16u;
+        en = lds128(qa);
+      }
     }
     uint32_t mask = en.x, kw = en.y, ow = en.w;
     for (int k = s - static_cast<int>(en.z); k > 0; --k) mask ^= 1u << top_bit(mask);
@@ -286,6 +343,7 @@ struct Ctx {
   uint32_t kf;      // smem: forcing keys of the band
   uint32_t lsm;     // smem: walk list
   uint32_t osm;     // smem: walk result words
+  uint32_t stage;   // smem: output staging (the TMA store source)
   uint64_t thr;
 };
 
@@ -294,7 +352,8 @@ struct Ctx {
 template <int NW, bool FORCE, int Q>
 __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
                                          const Ctx<NW, FORCE>& cx, int lane, uint32_t y,
-                                         uint32_t* out_row, int plane_words, int pad,
+                                         const CUtensorMap* stmap, const CUtensorMap* padmap,
+                                         int w0, int trow, int pad, int padx,
                                          bool pad_band, unsigned& swaps) {
   using G = Geo<NW, FORCE>;
   constexpr int P = G::kPlane;
@@ -317,6 +376,10 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
     K[w] = fhp3_classify(a, rr[w], so[w]);
     dep[w] = K[w].dep;
   }
+  // The previous row's TMA store must have read the staging area (which
+  // also holds the walk scratch) before it is rewritten.
+  if (lane == 0) bulk_wait_read();
+  __syncwarp();
   // Chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y)
   // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76).
   const int T = walk<NW>(dep, cx.lsm, cx.osm, cx.kc, lane,
@@ -356,13 +419,25 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
     uint32_t v[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) v[w] = o[w][p];
-    stv<NW>(out_row + p * plane_words, v);
-    if (pad_band && pad != 0) stv<NW>(out_row + p * plane_words + pad, v);  // periodic wrap copy
+    stsv<NW>(cx.stage + p * (4 * 32 * NW) + lane * NW * 4, v);
+    // periodic wrap copies: lanes holding words 0..3 / WW-4..WW-1
+    if (pad_band && pad >= 0) stsv<NW>(cx.stage + pad + p * 16, v);
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store(stmap, w0 + 4, trow, cx.stage);
+    if (pad_band) {
+      if (padx & 1) tma_store(padmap, 0, trow, cx.stage + Geo<NW, FORCE>::kPadL);
+      if (padx & 2) tma_store(padmap, (padx >> 2) + 4, trow, cx.stage + Geo<NW, FORCE>::kPadR);
+    }
+    bulk_commit();
   }
 }
 
 template <int NW, bool FORCE, int Q0>
 __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap* map,
+                                            const CUtensorMap* stmap, const CUtensorMap* padmap,
                                             const Lanes& L, uint32_t ring, uint32_t bars,
                                             const Ctx<NW, FORCE>& cx, int r_begin, int r_end,
                                             unsigned& swaps) {
@@ -393,15 +468,13 @@ __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap
   wait(sm);
   wait(sc);
   const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
-  uint32_t* out = reinterpret_cast<uint32_t*>(a.dst + r_begin * pitch) + 4 + L.w0 + L.lane * NW;
-  const long long pw = pitch / 4;
+  (void)pitch;
   auto one = [&](int r, auto qc) {
     constexpr int Q = decltype(qc)::value;
     wait(sn);
     dest_row<NW, FORCE, Q>(ring + sm * G::kSlot + lane_off, ring + sc * G::kSlot + lane_off,
-                           ring + sn * G::kSlot + lane_off, cx, L.lane, y0 + r, out, L.PW, L.pad,
-                           L.pad_band, swaps);
-    out += pw;
+                           ring + sn * G::kSlot + lane_off, cx, L.lane, y0 + r, stmap, padmap,
+                           L.w0, r + 1, L.pad, L.padx, L.pad_band, swaps);
     // The slot of row r-1 is free once every lane has read it.
     __syncwarp();
     if (issue_row <= last) {
@@ -418,11 +491,14 @@ __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap
     one(r + 1, std::integral_constant<int, Q0 ^ 1>{});
   }
   if (r < r_end) one(r, std::integral_constant<int, Q0>{});
+  if (L.lane == 0) bulk_wait_all();  // the stores have landed before the kernel ends
 }
 
 template <int NW, bool FORCE>
-__global__ void __launch_bounds__(kPThreads, 1)
-    step_planes_kernel(StepArgs a, const __grid_constant__ CUtensorMap map) {
+__global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
+    step_planes_kernel(StepArgs a, const __grid_constant__ CUtensorMap map,
+                       const __grid_constant__ CUtensorMap stmap,
+                       const __grid_constant__ CUtensorMap padmap) {
   using G = Geo<NW, FORCE>;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
@@ -437,9 +513,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const uint32_t kf_base = sbase + cta_cols * 8;
   const uint32_t wbase = sbase + (FORCE ? 2 : 1) * cta_cols * 8 + warp * G::kWarp;
   const uint32_t ring = wbase;
-  const uint32_t lsm = ring + G::kSlots * G::kSlot;
+  const uint32_t stage = ring + G::kSlots * G::kSlot;
+  const uint32_t lsm = stage;
   const uint32_t osm = lsm + G::kList;
-  const uint32_t bars = osm + G::kOut;
+  const uint32_t bars = stage + G::kStageAll;
   if ((threadIdx.x & 31) == 0) {
     for (int k = 0; k < G::kSlots; ++k) mbar_init(bars + k * 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -470,21 +547,25 @@ __global__ void __launch_bounds__(kPThreads, 1)
   L.WW = a.W >> 5;
   L.PW = L.WW + 8;
   L.w0 = band * G::kBandWords;
-  // Lanes holding words 0..3 / WW-4..WW-1 also write the right / left pad.
+  // Lanes holding words 0..3 / WW-4..WW-1 also stage the right / left pad
+  // box (periodic wrap copies): words 0..3 go to padded words WW+4..WW+7,
+  // words WW-4..WW-1 to padded words 0..3.
   const int wl = L.w0 + L.lane * NW;
-  L.pad = wl < 4 ? L.WW : (wl >= L.WW - 4 ? -L.WW : 0);
+  L.pad = wl < 4 ? G::kPadR + wl * 4 : (wl >= L.WW - 4 ? G::kPadL + (wl - (L.WW - 4)) * 4 : -1);
+  L.padx = (L.w0 + G::kBandWords == L.WW ? 1 : 0) | (L.w0 == 0 ? 2 : 0) | (L.WW << 2);
   L.pad_band = L.w0 == 0 || L.w0 + G::kBandWords == L.WW;
   Ctx<NW, FORCE> cx;
   cx.kc = kc_base + bic * G::kBandCols * 8;
   cx.kf = kf_base + bic * G::kBandCols * 8;
   cx.lsm = lsm;
   cx.osm = osm;
+  cx.stage = stage;
   cx.thr = a.thr;
   unsigned swaps = 0;
   if ((a.row0 + r_begin) & 1)
-    run_segment<NW, FORCE, 1>(a, &map, L, ring, bars, cx, r_begin, r_end, swaps);
+    run_segment<NW, FORCE, 1>(a, &map, &stmap, &padmap, L, ring, bars, cx, r_begin, r_end, swaps);
   else
-    run_segment<NW, FORCE, 0>(a, &map, L, ring, bars, cx, r_begin, r_end, swaps);
+    run_segment<NW, FORCE, 0>(a, &map, &stmap, &padmap, L, ring, bars, cx, r_begin, r_end, swaps);
   if (FORCE) {
     unsigned long long s = swaps;
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
@@ -495,21 +576,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
 template <int NW, bool FORCE>
 int smem_bytes(int bpc) {
   using G = Geo<NW, FORCE>;
-  return (FORCE ? 2 : 1) * bpc * G::kBandCols * 8 + kPWarps * G::kWarp;
+  return (FORCE ? 2 : 1) * bpc * G::kBandCols * 8 + kPWarps<NW> * G::kWarp;
 }
 
 template <int NW, bool FORCE>
-void launch_nw(StepArgs a, const CUtensorMap& map, int num_sms, cudaStream_t st) {
+void launch_nw(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st) {
   using G = Geo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
   a.nbands = a.W / G::kBandCols;
   // Bands per CTA: as many as the shared-memory budget allows (the column
   // keys of every band a CTA covers are staged).
-  int bpc = a.nbands < kPWarps ? a.nbands : kPWarps;
-  while (bpc > 1 && smem_bytes<NW, FORCE>(bpc) > 227 * 1024) bpc >>= 1;
-  while (kPWarps % bpc) --bpc;
+  constexpr int kWarps = kPWarps<NW>;
+  int bpc = a.nbands < kWarps ? a.nbands : kWarps;
+  while (bpc > 1 && smem_bytes<NW, FORCE>(bpc) > 226 * 1024) bpc >>= 1;
+  while (kWarps % bpc) --bpc;
   a.bpc = bpc;
-  a.spc = kPWarps / bpc;
+  a.spc = kWarps / bpc;
   a.nbands_groups = (a.nbands + bpc - 1) / bpc;
   int seg_groups = num_sms / a.nbands_groups;
   if (seg_groups < 1) seg_groups = 1;
@@ -520,13 +602,15 @@ void launch_nw(StepArgs a, const CUtensorMap& map, int num_sms, cudaStream_t st)
   seg_groups = (nseg + a.spc - 1) / a.spc;
   const int grid = a.nbands_groups * seg_groups;
   const int smem = smem_bytes<NW, FORCE>(bpc);
-  static bool attr = false;
-  if (!attr) {
+  // (The kernel also holds 1 KB of static shared memory for the bulk-copy
+  // machinery, so the dynamic opt-in is set to exactly what is used.)
+  static int attr = -1;
+  if (attr != smem) {
     cudaFuncSetAttribute(step_planes_kernel<NW, FORCE>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = smem;
   }
-  step_planes_kernel<NW, FORCE><<<grid, kPThreads, smem, st>>>(a, map);
+  step_planes_kernel<NW, FORCE><<<grid, kWarps * 32, smem, st>>>(a, maps[0], maps[1], maps[2]);
 }
 
 // ---------------------------------------------------------------------------
@@ -613,6 +697,7 @@ int grid_for(long long n, int num_sms) {
 int planes_words_per_lane(int W) {
   if (W <= 0 || W % 1024) return 0;
   const int bands1 = W / 1024;
+  if (bands1 % 4 == 0) return FHPG_PLANES_NW4;
   if (bands1 % 2 == 0) return 2;
   return 1;
 }
@@ -621,7 +706,7 @@ bool planes_ok(int W) { return planes_words_per_lane(W) != 0; }
 
 size_t planes_row_bytes(int W) { return static_cast<size_t>(W) + 256; }
 
-bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows) {
+bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows, int kind) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     void* fn = nullptr;
@@ -631,14 +716,16 @@ bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows)
       return false;
     encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
   }
-  // {padded words, planes, rows}; box {72 words, 8 planes, 1 row} (one band
-  // of 64 words + 4 on each side; NW = 1 bands of 32 words use {40, 8, 1}).
+  // Tensor {padded words, planes, rows}. Boxes: kind 0 (load) one band of
+  // 32 NW words + 4 on each side, all 8 planes; kind 1 (store) the band's
+  // words, planes 0-6; kind 2 (pad store) 4 words, planes 0-6.
   const int nw = planes_words_per_lane(W);
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(W / 32 + 8), 8,
                               static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>((W / 32 + 8) * 4),
                                  static_cast<cuuint64_t>(pitch)};
-  const cuuint32_t box[3] = {static_cast<cuuint32_t>(32 * nw + 8), 8, 1};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(kind == 0 ? 32 * nw + 8 : kind == 1 ? 32 * nw : 4),
+                             kind == 0 ? 8u : 7u, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode(static_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
                             buffer, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -647,11 +734,17 @@ bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows)
   return r == CUDA_SUCCESS;
 }
 
-int launch_step_planes(const StepArgs& a, const void* tmap_src, int num_sms, cudaStream_t st) {
+int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap_dst_store,
+                       const void* tmap_dst_pad, int num_sms, cudaStream_t st) {
   const int nw = planes_words_per_lane(a.W);
   const bool force = a.thr != 0;
-  const CUtensorMap& m = *static_cast<const CUtensorMap*>(tmap_src);
-  if (nw == 2) {
+  const CUtensorMap m[3] = {*static_cast<const CUtensorMap*>(tmap_src),
+                            *static_cast<const CUtensorMap*>(tmap_dst_store),
+                            *static_cast<const CUtensorMap*>(tmap_dst_pad)};
+  if (nw == 4) {
+    if (force) launch_nw<4, true>(a, m, num_sms, st);
+    else launch_nw<4, false>(a, m, num_sms, st);
+  } else if (nw == 2) {
     if (force) launch_nw<2, true>(a, m, num_sms, st);
     else launch_nw<2, false>(a, m, num_sms, st);
   } else {
