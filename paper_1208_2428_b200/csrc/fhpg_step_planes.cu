@@ -55,8 +55,17 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 // Warps per CTA (one CTA per SM): 16 with 2 words per lane, 8 with 4.
+#ifndef FHPG_PLANES_RING
+#define FHPG_PLANES_RING 1
+#endif
+#ifndef FHPG_PLANES_WARPS
+#define FHPG_PLANES_WARPS 16
+#endif
+#ifndef FHPG_PLANES_SLOTS
+#define FHPG_PLANES_SLOTS 4
+#endif
 template <int NW>
-constexpr int kPWarps = NW == 4 ? 8 : 16;
+constexpr int kPWarps = NW == 4 ? 8 : FHPG_PLANES_WARPS;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -176,7 +185,7 @@ struct Geo {
   static constexpr int kBandCols = 1024 * NW;
   static constexpr int kPlane = 32 + 4 * kBandWords;
   static constexpr int kSlot = 8 * kPlane;
-  static constexpr int kSlots = 4;
+  static constexpr int kSlots = FHPG_PLANES_SLOTS;
   // Output staging (7 planes x band words, the TMA store source) followed by
   // the two pad boxes (7 x 4 words each). The walk's list and result words
   // reuse the staging area: they are dead before the row's outputs land.
@@ -573,6 +582,172 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-shared row ring (default). One CTA = one band x a segment of rows; a
+// producer warp streams the segment's source rows into a ring of kRing
+// slots with TMA (full barriers), kCons consumer warps take destination rows
+// round-robin (warp k: rows R0 + k, R0 + k + kCons, ...), read their three
+// source rows from the shared ring and release them (empty barriers, 3
+// consumers per source row). Sharing the ring lets 20 warps per SM stream
+// with a deep prefetch in the shared-memory budget that per-warp rings
+// spend on 16.
+// ---------------------------------------------------------------------------
+// Consumer warps per CTA and ring slots (A/B on cfg4: 16/36 1570, 20/44
+// 1695, 24/52 1766, 30/64 1876, 31/48 1889 GSUPS).
+#ifndef FHPG_RING_CONS
+#define FHPG_RING_CONS 31
+#endif
+template <int NW, bool FORCE>
+struct RingGeo {
+  using G = Geo<NW, FORCE>;
+  static constexpr int kCons = FHPG_RING_CONS;
+#ifdef FHPG_RING_SLOTS
+  static constexpr int kRing = FHPG_RING_SLOTS;
+#else
+  static constexpr int kRing = FORCE ? 56 : 64;  // as many as the 227 KB allow
+#endif
+  static constexpr int kThreads = (kCons + 1) * 32;
+  static constexpr int kKeys = (FORCE ? 2 : 1) * G::kBandCols * 8;
+  static constexpr int kRingOff = (kKeys + 127) / 128 * 128;
+  static constexpr int kStageOff = kRingOff + kRing * G::kSlot;
+  static constexpr int kBarOff = kStageOff + kCons * G::kStageAll;
+  static constexpr int kSmem = kBarOff + 2 * 8 * kRing;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+template <int NW, bool FORCE>
+__global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
+    step_ring_kernel(StepArgs a, const __grid_constant__ CUtensorMap map,
+                     const __grid_constant__ CUtensorMap stmap,
+                     const __grid_constant__ CUtensorMap padmap) {
+  using G = Geo<NW, FORCE>;
+  using RG = RingGeo<NW, FORCE>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int band = blockIdx.x % a.nbands;
+  const int seg_group = blockIdx.x / a.nbands;
+  const int x0 = band * G::kBandCols;
+  const uint32_t kc_base = sbase;
+  const uint32_t kf_base = sbase + G::kBandCols * 8;
+  const uint32_t ring = sbase + RG::kRingOff;
+  const uint32_t full = sbase + RG::kBarOff;
+  const uint32_t empty = full + 8 * RG::kRing;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < RG::kRing; ++k) {
+      mbar_init(full + k * 8, 1);
+      mbar_init(empty + k * 8, 3);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int c = threadIdx.x; c < G::kBandCols; c += blockDim.x) {
+    sts64(kc_base + c * 8, a.zc[x0 + c]);
+    if (FORCE) sts64(kf_base + c * 8, a.zf[x0 + c]);
+  }
+  if (a.zc_next) {  // next step's column keys (read by the next launch only)
+    const int n = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.W; i += n) {
+      a.zc_next[i] = column_key(a.kc_next, static_cast<uint64_t>(i) + 1);
+      if (a.zf_next) a.zf_next[i] = column_key(a.kf_next, static_cast<uint64_t>(i) + 1);
+    }
+  }
+  __syncthreads();
+  const int R0 = a.row_lo + seg_group * a.seg_rows;
+  const int R1 = min(a.row_hi, R0 + a.seg_rows);
+  if (R0 >= R1) return;
+  const int w0 = band * G::kBandWords;
+
+  if (warp == RG::kCons) {  // producer: source rows R0-1 .. R1 (tensor row = local + 1)
+    if (lane == 0) {
+      for (int s = R0 - 1, i = 0; s <= R1; ++s, ++i) {
+        const int k = i % RG::kRing;
+        if (i >= RG::kRing) mbar_wait(empty + k * 8, static_cast<uint32_t>((i / RG::kRing - 1) & 1));
+        mbar_expect_tx(full + k * 8, G::kRowBytes);
+        tma_row(ring + k * G::kSlot, &map, w0, s + 1, full + k * 8);
+      }
+    }
+    return;
+  }
+
+  Lanes L;
+  L.lane = lane;
+  L.WW = a.W >> 5;
+  L.PW = L.WW + 8;
+  L.w0 = w0;
+  const int wl = L.w0 + L.lane * NW;
+  L.pad = wl < 4 ? G::kPadR + wl * 4 : (wl >= L.WW - 4 ? G::kPadL + (wl - (L.WW - 4)) * 4 : -1);
+  L.padx = (L.w0 + G::kBandWords == L.WW ? 1 : 0) | (L.w0 == 0 ? 2 : 0) | (L.WW << 2);
+  L.pad_band = L.w0 == 0 || L.w0 + G::kBandWords == L.WW;
+  const uint32_t stage = sbase + RG::kStageOff + warp * G::kStageAll;
+  Ctx<NW, FORCE> cx;
+  cx.kc = kc_base;
+  cx.kf = kf_base;
+  cx.lsm = stage;
+  cx.osm = stage + G::kList;
+  cx.stage = stage;
+  cx.thr = a.thr;
+  unsigned swaps = 0;
+  const uint32_t lane_off = 16u + lane * NW * 4u;
+  const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
+  for (int r = R0 + warp; r < R1; r += RG::kCons) {
+    const int i = r - R0;  // ring index of source row r - 1
+    uint32_t sl[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int k = (i + d) % RG::kRing;
+      mbar_wait(full + k * 8, static_cast<uint32_t>(((i + d) / RG::kRing) & 1));
+      sl[d] = ring + k * G::kSlot + lane_off;
+    }
+    if ((a.row0 + r) & 1)
+      dest_row<NW, FORCE, 1>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
+                             L.pad, L.padx, L.pad_band, swaps);
+    else
+      dest_row<NW, FORCE, 0>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
+                             L.pad, L.padx, L.pad_band, swaps);
+    // Release the three source rows (3 consumers each; segment edges make
+    // up for the destination rows outside [R0, R1)).
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t first = r == R0 ? 1u : 0u, lastr = r == R1 - 1 ? 1u : 0u;
+      mbar_arrive(empty + ((i) % RG::kRing) * 8, 1 + 2 * first);
+      mbar_arrive(empty + ((i + 1) % RG::kRing) * 8, 1 + first + lastr);
+      mbar_arrive(empty + ((i + 2) % RG::kRing) * 8, 1 + 2 * lastr);
+    }
+  }
+  if (lane == 0) bulk_wait_all();  // the stores have landed before the kernel ends
+  if (FORCE) {
+    unsigned long long sw = swaps;
+    for (int o = 16; o; o >>= 1) sw += __shfl_xor_sync(kFull, sw, o);
+    if (lane == 0 && sw) atomicAdd(a.swaps, sw);
+  }
+}
+
+template <int NW, bool FORCE>
+void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st) {
+  using G = Geo<NW, FORCE>;
+  using RG = RingGeo<NW, FORCE>;
+  const int rows = a.row_hi - a.row_lo;
+  a.nbands = a.W / G::kBandCols;
+  int seg_groups = num_sms / a.nbands;
+  if (seg_groups < 1) seg_groups = 1;
+  int seg = (rows + seg_groups - 1) / seg_groups;
+  if (seg < 1) seg = 1;
+  a.seg_rows = seg;
+  seg_groups = (rows + seg - 1) / seg;
+  const int grid = a.nbands * seg_groups;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(step_ring_kernel<NW, FORCE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         RG::kSmem);
+    attr = true;
+  }
+  step_ring_kernel<NW, FORCE><<<grid, RG::kThreads, RG::kSmem, st>>>(a, maps[0], maps[1], maps[2]);
+}
+
 template <int NW, bool FORCE>
 int smem_bytes(int bpc) {
   using G = Geo<NW, FORCE>;
@@ -741,6 +916,13 @@ int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap
   const CUtensorMap m[3] = {*static_cast<const CUtensorMap*>(tmap_src),
                             *static_cast<const CUtensorMap*>(tmap_dst_store),
                             *static_cast<const CUtensorMap*>(tmap_dst_pad)};
+#if FHPG_PLANES_RING
+  if (nw == 2) {
+    if (force) launch_ring<2, true>(a, m, num_sms, st);
+    else launch_ring<2, false>(a, m, num_sms, st);
+    return 1;
+  }
+#endif
   if (nw == 4) {
     if (force) launch_nw<4, true>(a, m, num_sms, st);
     else launch_nw<4, false>(a, m, num_sms, st);
