@@ -64,7 +64,8 @@ constexpr uint32_t kRedSingle = FHPG_LUT((kLC & ~kLA & kLB) | (~kLC & kLA & ~kLB
 // FHP-III, phase 1 output: class masks kept across the chirality walk.
 struct Fhp3Class {
   uint32_t D;      // sites with mass >= 4 (complemented)
-  uint32_t ROT, BB, X, B, AY, Y, KEEP, xp;
+  uint32_t ROT, BB, X, B, AY, KEEP, xp;
+  uint32_t YE[3];  // Y sites whose axis m is empty (no odd mover)
   uint32_t dep;
 };
 
@@ -96,19 +97,22 @@ FHPG_HD Fhp3Class fhp3_classify(const uint32_t a[6], uint32_t r, uint32_t s) {
   k.X = exf1 & anyP;
   k.B = lop3<FHPG_LUT(kLA & ~kLB & kLC)>(exf1, anyP, rp);
   // Two odd axes with movers 120 deg apart <=> both on directions of the
-  // same parity <=> an even number of odd-direction singles (invariant).
-  const uint32_t v1 = a[1] & ~a[4], v3 = a[3] & ~a[0], v5 = a[5] & ~a[2];
-  const uint32_t pi = lop3<kXor3>(v1, v3, v5);
+  // same parity <=> an even number of singles on odd directions. With two
+  // odd axes the third axis is empty (reduced), i.e. a pair when D = 1, so
+  // that parity is a1 ^ a3 ^ a5 ^ D.
+  const uint32_t pi = lop3<kXor3>(a[1], a[3], a[5]) ^ D;
   k.AY = lop3<FHPG_LUT(kLA & ~kLB & ~kLC)>(ex2, pi, s);
-  k.Y = k.AY & rp;
+  const uint32_t Y = k.AY & rp;
+  k.YE[0] = Y & ~O0;
+  k.YE[1] = Y & ~O1;
+  k.YE[2] = Y & ~O2;
   const uint32_t t = lop3<kOr3>(k.ROT, k.X, k.B);
   k.KEEP = lop3<kNor3>(t, k.BB, k.AY);
-  // X states: the pair's axis follows the odd axis (X+) or precedes it (X-).
-  const uint32_t x1 = O0 & P1;
-  const uint32_t x2 = lop3<kAndOr>(O1, P2, x1);
-  k.xp = lop3<kAndOr>(O2, P0, x2);
+  // X states (one odd axis o, one pair): the pair's axis is o + 1 (X+) or
+  // o - 1 (X-).
+  k.xp = lop3<kMux>(O0, P1, lop3<kMux>(O1, P2, P0));
   const uint32_t d1 = lop3<kAndOr>(k.ROT, anyP, k.X);
-  k.dep = d1 | k.Y;
+  k.dep = d1 | Y;
   return k;
 }
 
@@ -125,19 +129,15 @@ FHPG_HD void fhp3_apply(const Fhp3Class& k, uint32_t c, uint32_t r, const uint32
   // are complemented back with D.
   const uint32_t S3 = k.BB | NX;
   const uint32_t DN = lop3<FHPG_LUT(kLA | (kLB & kLC))>(NX, k.D, UAY);
-  uint32_t v[6], g[6];
+  uint32_t v[6];
 #pragma unroll
-  for (int i = 0; i < 6; ++i) {
+  for (int i = 0; i < 6; ++i)
     v[i] = lop3<kRedSingle>(a[i], a[(i + 3) % 6], k.D);  // reduced: odd mover of its axis
-    g[i] = lop3<kRedAnd>(a[i], a[(i + 4) % 6], k.D);     // reduced: a_i & a_{i-2}
-  }
-  // Y -> X: the pair lands on the axis of the mover whose partner sits at
-  // -120 deg (c = 0) or +120 deg (c = 1).
-  uint32_t GY[3], PA[3];
+  // Y = {j-1, j+1} + R -> X: the pair lands on the axis of j+1 (c = 0) or
+  // j-1 (c = 1), i.e. one (c = 0: two) axes after the empty axis j.
+  uint32_t PA[3];
 #pragma unroll
-  for (int m = 0; m < 3; ++m) GY[m] = lop3<FHPG_LUT(kLA & (kLB | kLC))>(k.Y, g[m], g[m + 3]);
-#pragma unroll
-  for (int m = 0; m < 3; ++m) PA[m] = lop3<kMux>(c, GY[(m + 2) % 3], GY[m]);
+  for (int m = 0; m < 3; ++m) PA[m] = lop3<kMux>(c, k.YE[(m + 1) % 3], k.YE[(m + 2) % 3]);
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     const uint32_t rot = lop3<kMux>(c, a[(i + 5) % 6], a[(i + 1) % 6]);
