@@ -240,7 +240,9 @@ def main():
                          "W": W_LAT, "H": H, "rows_per_gpu": H_PER_GPU, "table": "FHP-III",
                          "parallelism": f"row-strips x{world}" if world > 1 else "single",
                          "l2": "inputs larger than L2 (2 x 268 MB state buffers per GPU)",
-                         "kernel": "fast" if eng.fast_path else "generic"},
+                         "kernel": {"planes": "bit-plane ring kernel (step_ring_kernel)",
+                                    "bytes": "byte streaming kernel (step_fast_kernel)",
+                                    "generic": "generic"}[eng.path]},
               "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                            "frac": achieved / peak, "traffic": traffic,
                            "bytes_per_site": BYTES_PER_SITE, "peak_source": peak_src,
