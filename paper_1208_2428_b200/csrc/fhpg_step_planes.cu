@@ -611,7 +611,8 @@ struct RingGeo {
   static constexpr int kRingOff = (kKeys + 127) / 128 * 128;
   static constexpr int kStageOff = kRingOff + kRing * G::kSlot;
   static constexpr int kBarOff = kStageOff + kCons * G::kStageAll;
-  static constexpr int kSmem = kBarOff + 2 * 8 * kRing;
+  static constexpr int kTagOff = kBarOff + 2 * 8 * kRing;
+  static constexpr int kSmem = kTagOff + 4 * kRing;
 };
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar, uint32_t count) {
@@ -637,10 +638,16 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   const uint32_t ring = sbase + RG::kRingOff;
   const uint32_t full = sbase + RG::kBarOff;
   const uint32_t empty = full + 8 * RG::kRing;
+  // tag[k] = ring index of the row the producer last issued into slot k. A
+  // consumer visits only every kCons-th row, so a bare parity wait could
+  // mistake a slot two phases old for the one it needs; it first waits for
+  // the tag, after which the full barrier's parity is unambiguous.
+  const uint32_t tags = sbase + RG::kTagOff;
   if (threadIdx.x == 0) {
     for (int k = 0; k < RG::kRing; ++k) {
       mbar_init(full + k * 8, 1);
       mbar_init(empty + k * 8, 3);
+      sts32(tags + k * 4, 0xFFFFFFFFu);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -666,6 +673,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
       for (int s = R0 - 1, i = 0; s <= R1; ++s, ++i) {
         const int k = i % RG::kRing;
         if (i >= RG::kRing) mbar_wait(empty + k * 8, static_cast<uint32_t>((i / RG::kRing - 1) & 1));
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(tags + k * 4), "r"(i) : "memory");
         mbar_expect_tx(full + k * 8, G::kRowBytes);
         tma_row(ring + k * G::kSlot, &map, w0, s + 1, full + k * 8);
       }
@@ -699,6 +707,12 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const int k = (i + d) % RG::kRing;
+      for (;;) {
+        uint32_t tag;
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tag) : "r"(tags + k * 4) : "memory");
+        if (tag == static_cast<uint32_t>(i + d)) break;
+        __nanosleep(64);
+      }
       mbar_wait(full + k * 8, static_cast<uint32_t>(((i + d) / RG::kRing) & 1));
       sl[d] = ring + k * G::kSlot + lane_off;
     }
