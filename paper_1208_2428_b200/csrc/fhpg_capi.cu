@@ -27,7 +27,7 @@ struct fhpg_engine {
   bool table_planes = false;
   int path_pref = 0;                     // 0 auto, 1 byte fast path, 2 generic
   uint8_t* scratch = nullptr;            // nrows * pitch
-  alignas(64) unsigned char tmap[2][3][128];  // TMA descriptors of buf[0], buf[1] (planes)
+  alignas(64) unsigned char tmap[2][4][128];  // TMA descriptors of buf[0], buf[1] (planes)
   bool scratch_valid = false;
   uint8_t* table = nullptr;              // 512 bytes
   uint64_t* zkeys = nullptr;             // [parity][purpose][W]
@@ -143,7 +143,7 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
     for (int i = 0; i < 2; ++i) {
       ck(cudaMalloc(&e->buf[i], bytes), "cudaMalloc(state)");
       ck(cudaMemset(e->buf[i], 0, bytes), "cudaMemset(state)");
-      for (int kind = 0; kind < 3 && fhpg::planes_ok(W); ++kind)
+      for (int kind = 0; kind < 4 && fhpg::planes_ok(W); ++kind)
         if (!fhpg::make_planes_map(e->tmap[i][kind], e->buf[i], W, e->pitch, e->nrows + 5, kind))
           throw Failure{FHPG_ERUNTIME, "cuTensorMapEncodeTiled failed"};
     }
@@ -224,7 +224,8 @@ void launch_any(fhpg_engine* e, const fhpg::StepArgs& a) {
   if (e->planes) {
     const int which = a.src == e->base(0) ? 0 : 1;
     e->launches += fhpg::launch_step_planes(a, e->tmap[which][0], e->tmap[which ^ 1][1],
-                                            e->tmap[which ^ 1][2], e->num_sms, e->stream);
+                                            e->tmap[which ^ 1][2], e->tmap[which][3],
+                                            e->num_sms, e->stream);
     e->scratch_valid = false;
   } else {
     e->launches += fhpg::launch_step(a, e->num_sms, e->stream, e->path_pref == 2);

@@ -55,13 +55,14 @@ size_t planes_row_bytes(int W);
 // TMA descriptor (CUtensorMap, 64-byte aligned, 128 bytes) of a plane buffer
 // whose row 0 is at `buffer` (the top halo row), `rows` rows; kind 0 = row
 // loads (band + edge words, 8 planes), 1 = band stores (7 planes), 2 = pad
-// stores (4 words, 7 planes).
+// stores (4 words, 7 planes), 3 = two-row loads.
 bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows, int kind);
 // One time step with the FHP-III circuit over rows [row_lo, row_hi): loads
 // through the source buffer's kind-0 map, stores through the destination
 // buffer's kind-1 / kind-2 maps.
 int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap_dst_store,
-                       const void* tmap_dst_pad, int num_sms, cudaStream_t st);
+                       const void* tmap_dst_pad, const void* tmap_src_pair, int num_sms,
+                       cudaStream_t st);
 // Bytes (rows 0..nrows-1 of src) -> planes in dst; plane 7 from the mask,
 // also written into dst_obst (the other ping-pong buffer).
 void launch_pack_planes(const uint8_t* src, const uint8_t* mask, uint8_t* dst, uint8_t* dst_obst,

@@ -358,12 +358,14 @@ struct Ctx {
 
 // One destination row. sm, sc, sn: this lane's word address inside plane 0
 // of the slots of rows r-1, r, r+1; Q = global parity of r.
-template <int NW, bool FORCE, int Q>
+// `released()` is called once the source rows have been read into
+// registers (the ring slots may be refilled from then on).
+template <int NW, bool FORCE, int Q, typename Rel>
 __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
                                          const Ctx<NW, FORCE>& cx, int lane, uint32_t y,
                                          const CUtensorMap* stmap, const CUtensorMap* padmap,
                                          int w0, int trow, int pad, int padx,
-                                         bool pad_band, unsigned& swaps) {
+                                         bool pad_band, unsigned& swaps, Rel&& released) {
   using G = Geo<NW, FORCE>;
   constexpr int P = G::kPlane;
   uint32_t a0[NW], a1[NW], a2[NW], a3[NW], a4[NW], a5[NW], rr[NW], so[NW];
@@ -377,6 +379,7 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   rd_shr<NW>(sc + 5 * P, a5);
   rd_al<NW>(sc + 6 * P, rr);
   rd_al<NW>(sc + 7 * P, so);
+  released();
   Fhp3Class K[NW];
   uint32_t dep[NW];
 #pragma unroll
@@ -483,7 +486,7 @@ __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap
     wait(sn);
     dest_row<NW, FORCE, Q>(ring + sm * G::kSlot + lane_off, ring + sc * G::kSlot + lane_off,
                            ring + sn * G::kSlot + lane_off, cx, L.lane, y0 + r, stmap, padmap,
-                           L.w0, r + 1, L.pad, L.padx, L.pad_band, swaps);
+                           L.w0, r + 1, L.pad, L.padx, L.pad_band, swaps, [] {});
     // The slot of row r-1 is free once every lane has read it.
     __syncwarp();
     if (issue_row <= last) {
@@ -613,6 +616,7 @@ struct RingGeo {
   static constexpr int kBarOff = kStageOff + kCons * G::kStageAll;
   static constexpr int kTagOff = kBarOff + 2 * 8 * kRing;
   static constexpr int kSmem = kTagOff + 4 * kRing;
+  static_assert(kRing % 2 == 0, "row pairs");
 };
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar, uint32_t count) {
@@ -623,7 +627,8 @@ template <int NW, bool FORCE>
 __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
     step_ring_kernel(StepArgs a, const __grid_constant__ CUtensorMap map,
                      const __grid_constant__ CUtensorMap stmap,
-                     const __grid_constant__ CUtensorMap padmap) {
+                     const __grid_constant__ CUtensorMap padmap,
+                     const __grid_constant__ CUtensorMap map2) {
   using G = Geo<NW, FORCE>;
   using RG = RingGeo<NW, FORCE>;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -645,8 +650,10 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   const uint32_t tags = sbase + RG::kTagOff;
   if (threadIdx.x == 0) {
     for (int k = 0; k < RG::kRing; ++k) {
+      // Source rows come in pairs (one 2-row TMA box): pair P = index / 2
+      // uses barriers / tag P mod kRing/2 (count 6 = 3 consumers per row).
       mbar_init(full + k * 8, 1);
-      mbar_init(empty + k * 8, 3);
+      mbar_init(empty + k * 8, 6);
       sts32(tags + k * 4, 0xFFFFFFFFu);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -670,12 +677,14 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
 
   if (warp == RG::kCons) {  // producer: source rows R0-1 .. R1 (tensor row = local + 1)
     if (lane == 0) {
-      for (int s = R0 - 1, i = 0; s <= R1; ++s, ++i) {
-        const int k = i % RG::kRing;
-        if (i >= RG::kRing) mbar_wait(empty + k * 8, static_cast<uint32_t>((i / RG::kRing - 1) & 1));
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(tags + k * 4), "r"(i) : "memory");
-        mbar_expect_tx(full + k * 8, G::kRowBytes);
-        tma_row(ring + k * G::kSlot, &map, w0, s + 1, full + k * 8);
+      constexpr int kPairs = RG::kRing / 2;
+      const int npairs = (R1 - R0 + 3) / 2;  // rows R0-1 .. R1 (+ a spare zero row)
+      for (int P = 0; P < npairs; ++P) {
+        const int k = P % kPairs;
+        if (P >= kPairs) mbar_wait(empty + k * 8, static_cast<uint32_t>((P / kPairs - 1) & 1));
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(tags + k * 4), "r"(P) : "memory");
+        mbar_expect_tx(full + k * 8, 2 * G::kRowBytes);
+        tma_row(ring + 2 * k * G::kSlot, &map2, w0, R0 + 2 * P, full + k * 8);  // tensor rows
       }
     }
     return;
@@ -703,34 +712,41 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
   for (int r = R0 + warp; r < R1; r += RG::kCons) {
     const int i = r - R0;  // ring index of source row r - 1
+    constexpr int kPairs = RG::kRing / 2;
     uint32_t sl[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const int k = (i + d) % RG::kRing;
-      for (;;) {
-        uint32_t tag;
-        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tag) : "r"(tags + k * 4) : "memory");
-        if (tag == static_cast<uint32_t>(i + d)) break;
-        __nanosleep(64);
+      const int P = (i + d) >> 1;
+      if (d == 0 || ((i + d) & 1) == 0) {  // a new pair
+        const int kp = P % kPairs;
+        for (;;) {
+          uint32_t tag;
+          asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tag) : "r"(tags + kp * 4) : "memory");
+          if (tag == static_cast<uint32_t>(P)) break;
+          __nanosleep(64);
+        }
+        mbar_wait(full + kp * 8, static_cast<uint32_t>((P / kPairs) & 1));
       }
-      mbar_wait(full + k * 8, static_cast<uint32_t>(((i + d) / RG::kRing) & 1));
-      sl[d] = ring + k * G::kSlot + lane_off;
+      sl[d] = ring + ((i + d) % RG::kRing) * G::kSlot + lane_off;
     }
+    // Release the three source rows as soon as they are in registers (3
+    // consumers per row; segment edges make up for the destination rows
+    // outside [R0, R1)).
+    auto release = [&] {
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t first = r == R0 ? 1u : 0u, lastr = r == R1 - 1 ? 1u : 0u;
+        mbar_arrive(empty + (((i) >> 1) % kPairs) * 8, 1 + 2 * first);
+        mbar_arrive(empty + (((i + 1) >> 1) % kPairs) * 8, 1 + first + lastr);
+        mbar_arrive(empty + (((i + 2) >> 1) % kPairs) * 8, 1 + 2 * lastr);
+      }
+    };
     if ((a.row0 + r) & 1)
       dest_row<NW, FORCE, 1>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
-                             L.pad, L.padx, L.pad_band, swaps);
+                             L.pad, L.padx, L.pad_band, swaps, release);
     else
       dest_row<NW, FORCE, 0>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
-                             L.pad, L.padx, L.pad_band, swaps);
-    // Release the three source rows (3 consumers each; segment edges make
-    // up for the destination rows outside [R0, R1)).
-    __syncwarp();
-    if (lane == 0) {
-      const uint32_t first = r == R0 ? 1u : 0u, lastr = r == R1 - 1 ? 1u : 0u;
-      mbar_arrive(empty + ((i) % RG::kRing) * 8, 1 + 2 * first);
-      mbar_arrive(empty + ((i + 1) % RG::kRing) * 8, 1 + first + lastr);
-      mbar_arrive(empty + ((i + 2) % RG::kRing) * 8, 1 + 2 * lastr);
-    }
+                             L.pad, L.padx, L.pad_band, swaps, release);
   }
   if (lane == 0) bulk_wait_all();  // the stores have landed before the kernel ends
   if (FORCE) {
@@ -759,7 +775,8 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
                          RG::kSmem);
     attr = true;
   }
-  step_ring_kernel<NW, FORCE><<<grid, RG::kThreads, RG::kSmem, st>>>(a, maps[0], maps[1], maps[2]);
+  step_ring_kernel<NW, FORCE><<<grid, RG::kThreads, RG::kSmem, st>>>(a, maps[0], maps[1], maps[2],
+                                                                     maps[3]);
 }
 
 template <int NW, bool FORCE>
@@ -907,14 +924,16 @@ bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows,
   }
   // Tensor {padded words, planes, rows}. Boxes: kind 0 (load) one band of
   // 32 NW words + 4 on each side, all 8 planes; kind 1 (store) the band's
-  // words, planes 0-6; kind 2 (pad store) 4 words, planes 0-6.
+  // words, planes 0-6; kind 2 (pad store) 4 words, planes 0-6; kind 3 (load)
+  // as kind 0 for two consecutive rows.
   const int nw = planes_words_per_lane(W);
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(W / 32 + 8), 8,
                               static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>((W / 32 + 8) * 4),
                                  static_cast<cuuint64_t>(pitch)};
-  const cuuint32_t box[3] = {static_cast<cuuint32_t>(kind == 0 ? 32 * nw + 8 : kind == 1 ? 32 * nw : 4),
-                             kind == 0 ? 8u : 7u, 1};
+  const cuuint32_t box[3] = {
+      static_cast<cuuint32_t>(kind == 0 || kind == 3 ? 32 * nw + 8 : kind == 1 ? 32 * nw : 4),
+      kind == 0 || kind == 3 ? 8u : 7u, kind == 3 ? 2u : 1u};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode(static_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
                             buffer, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -924,12 +943,14 @@ bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows,
 }
 
 int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap_dst_store,
-                       const void* tmap_dst_pad, int num_sms, cudaStream_t st) {
+                       const void* tmap_dst_pad, const void* tmap_src_pair, int num_sms,
+                       cudaStream_t st) {
   const int nw = planes_words_per_lane(a.W);
   const bool force = a.thr != 0;
-  const CUtensorMap m[3] = {*static_cast<const CUtensorMap*>(tmap_src),
+  const CUtensorMap m[4] = {*static_cast<const CUtensorMap*>(tmap_src),
                             *static_cast<const CUtensorMap*>(tmap_dst_store),
-                            *static_cast<const CUtensorMap*>(tmap_dst_pad)};
+                            *static_cast<const CUtensorMap*>(tmap_dst_pad),
+                            *static_cast<const CUtensorMap*>(tmap_src_pair)};
 #if FHPG_PLANES_RING
   if (nw == 2) {
     if (force) launch_ring<2, true>(a, m, num_sms, st);
