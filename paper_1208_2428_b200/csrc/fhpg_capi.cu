@@ -329,7 +329,15 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
     if (interior) run(1, e->nrows - 1, true);
     return;
   }
-  if (interior) {
+  if (interior && e->planes) {
+    // both boundary rows in one launch of the ring kernel
+    StepArgs b = a;
+    b.row_lo = 0;
+    b.row_hi = 1;
+    b.row_lo2 = e->nrows - 1;
+    b.row_hi2 = e->nrows;
+    launch_any(e, b);
+  } else if (interior) {
     run(0, 1, false);
     run(e->nrows - 1, e->nrows, false);
   } else {

@@ -38,6 +38,8 @@ struct StepArgs {
   int nbands_groups;         // CTA column groups (fast path)
   int bpc, spc;              // bands x segments per CTA (fast path)
   int row_lo, row_hi;        // local row range to update, [row_lo, row_hi)
+  int row_lo2 = 0, row_hi2 = 0;  // optional second range (bit-plane path: boundary rows)
+  int segs1 = 0;             // row segments of the first range (bit-plane ring kernel)
 };
 
 // Fast path launcher (fhpg_step_fast.cu).

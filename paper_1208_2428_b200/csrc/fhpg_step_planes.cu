@@ -636,7 +636,11 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int band = blockIdx.x % a.nbands;
-  const int seg_group = blockIdx.x / a.nbands;
+  // Segments of the first row range, then of the optional second one.
+  const bool second = static_cast<int>(blockIdx.x / a.nbands) >= a.segs1;
+  const int seg_group = blockIdx.x / a.nbands - (second ? a.segs1 : 0);
+  const int row_lo = second ? a.row_lo2 : a.row_lo;
+  const int row_hi = second ? a.row_hi2 : a.row_hi;
   const int x0 = band * G::kBandCols;
   const uint32_t kc_base = sbase;
   const uint32_t kf_base = sbase + G::kBandCols * 8;
@@ -670,8 +674,8 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
     }
   }
   __syncthreads();
-  const int R0 = a.row_lo + seg_group * a.seg_rows;
-  const int R1 = min(a.row_hi, R0 + a.seg_rows);
+  const int R0 = row_lo + seg_group * a.seg_rows;
+  const int R1 = min(row_hi, R0 + a.seg_rows);
   if (R0 >= R1) return;
   const int w0 = band * G::kBandWords;
 
@@ -768,7 +772,9 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
   if (seg < 1) seg = 1;
   a.seg_rows = seg;
   seg_groups = (rows + seg - 1) / seg;
-  const int grid = a.nbands * seg_groups;
+  a.segs1 = seg_groups;
+  const int rows2 = a.row_hi2 > a.row_lo2 ? a.row_hi2 - a.row_lo2 : 0;
+  const int grid = a.nbands * (seg_groups + (rows2 + seg - 1) / seg);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(step_ring_kernel<NW, FORCE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -958,6 +964,16 @@ int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap
     return 1;
   }
 #endif
+  if (a.row_hi2 > a.row_lo2) {  // per-warp-ring kernels take one range per launch
+    StepArgs a1 = a, a2 = a;
+    a1.row_lo2 = a1.row_hi2 = a2.row_lo2 = a2.row_hi2 = 0;
+    a2.row_lo = a.row_lo2;
+    a2.row_hi = a.row_hi2;
+    return launch_step_planes(a1, tmap_src, tmap_dst_store, tmap_dst_pad, tmap_src_pair, num_sms,
+                              st) +
+           launch_step_planes(a2, tmap_src, tmap_dst_store, tmap_dst_pad, tmap_src_pair, num_sms,
+                              st);
+  }
   if (nw == 4) {
     if (force) launch_nw<4, true>(a, m, num_sms, st);
     else launch_nw<4, false>(a, m, num_sms, st);

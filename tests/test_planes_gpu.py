@@ -159,7 +159,7 @@ def test_observables_in_planes_mode(port, tables):
 
 
 def test_split_steps_planes(port, tables):
-    for (W, H) in ((1024, 40), (2048, 3), (2048, 4)):
+    for (W, H) in ((1024, 40), (2048, 3), (2048, 4), (16384, 37)):
         s, m = port.scramble(W, H, 21)
         b = engine(W, H, tables["fhp3"], m, s)
         assert b.path == "planes"
