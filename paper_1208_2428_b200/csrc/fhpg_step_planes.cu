@@ -55,6 +55,9 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 // Warps per CTA (one CTA per SM): 16 with 2 words per lane, 8 with 4.
+#ifndef FHPG_STREAM_ONLY
+#define FHPG_STREAM_ONLY 0  // timing experiment: memory pipeline only (wrong results)
+#endif
 #ifndef FHPG_PLANES_RING
 #define FHPG_PLANES_RING 1
 #endif
@@ -380,6 +383,29 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   rd_al<NW>(sc + 6 * P, rr);
   rd_al<NW>(sc + 7 * P, so);
   released();
+#if FHPG_STREAM_ONLY
+  // Timing experiment only (wrong results): the memory pipeline without the
+  // collision and the chirality walk.
+  if (lane == 0) bulk_wait_read();
+  __syncwarp();
+#pragma unroll
+  for (int p = 0; p < 7; ++p) {
+    uint32_t v[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w)
+      v[w] = (p == 0 ? a0[w] : p == 1 ? a1[w] : p == 2 ? a2[w] : p == 3 ? a3[w] : p == 4 ? a4[w]
+              : p == 5 ? a5[w] : rr[w]) ^ so[w];
+    stsv<NW>(cx.stage + p * (4 * 32 * NW) + lane * NW * 4, v);
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store(stmap, w0 + 4, trow, cx.stage);
+    bulk_commit();
+  }
+  (void)swaps; (void)y; (void)pad; (void)padx; (void)pad_band; (void)padmap;
+  return;
+#endif
   Fhp3Class K[NW];
   uint32_t dep[NW];
 #pragma unroll
