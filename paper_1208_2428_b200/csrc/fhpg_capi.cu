@@ -1,7 +1,6 @@
 // fhpg_capi.cu — the C ABI (include/fhpg.h): engine object, device memory,
 // error mapping, and the step loop that drives the kernels.
 #include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -43,7 +42,6 @@ struct fhpg_engine {
   int64_t keys_step = -1;                // step whose column keys are in keys(step & 1)
   uint64_t keys_seed = 0;
   bool keys_force = false;
-  int rng_exact = 0;                     // FHPG_DEBUG_EXACT_RNG (test hook, StepArgs::rng_exact)
 
   uint8_t* base(int which) const { return buf[which] + pitch; }  // local row 0
   uint64_t* keys(int parity, int purpose) const {
@@ -138,10 +136,6 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
     e->row_end = re;
     e->nrows = re - rb;
     e->device = device;
-    {
-      const char* ex = std::getenv("FHPG_DEBUG_EXACT_RNG");
-      e->rng_exact = ex && ex[0] == '1' ? 1 : 0;
-    }
     // Room for the bit-plane rows (W + 256 bytes) when the width allows them.
     e->pitch = (static_cast<size_t>(W) + 15) / 16 * 16 + (fhpg::planes_ok(W) ? 256 : 0);
     // halo above, rows, halo below, 3 spare zero rows the streaming kernels may prefetch
@@ -268,7 +262,6 @@ void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64
     a.zf = force ? e->keys(s & 1, 1) : nullptr;
     a.thr = thr;
     a.swaps = e->swaps;
-    a.rng_exact = e->rng_exact;
     if (i + 1 < count) {
       a.zc_next = e->keys((s + 1) & 1, 0);
       a.zf_next = force ? e->keys((s + 1) & 1, 1) : nullptr;
@@ -319,7 +312,6 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
   a.zf = force ? e->keys(s & 1, 1) : nullptr;
   a.thr = thr;
   a.swaps = e->swaps;
-  a.rng_exact = e->rng_exact;
   const bool interior = e->nrows >= 3;
   auto run = [&](int lo, int hi, bool with_next_keys) {
     StepArgs b = a;

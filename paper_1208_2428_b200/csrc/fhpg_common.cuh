@@ -65,39 +65,25 @@ FHPG_HD uint32_t fin64_bit0(uint64_t z) {
   return (p ^ (p >> 31)) & 1u;
 }
 
-// The same bit with the column's share of the work precomputed (bit-plane
-// ring kernel). For z = K + y whose low word does not carry (lo32(K) + y <
-// 2^32, hi = hi32(K)):
-//   lo32(z ^ z >> 30) = lo ^ (lo >> 30) ^ (hi << 2),   lo = lo32(K) + y
-//   hi32(z ^ z >> 30) = hi ^ (hi >> 30)              (per column)
-//   z1 = (z ^ z >> 30) * C1 needs only lo32 * C1 plus G = hi32(..) * lo32(C1)
-//        added to its high word,
-// and bit0(p) ^ bit31(p) of p = lo32(z1 ^ z1 >> 27) * lo32(C2) is the sign
-// bit of p * (1 + 2^31) = lo32(z1 ^ z1 >> 27) * kC2s. Per column the kernel
-// stages {lo32(K), A = hi << 2, G}; `carry` (0/1) lets a column whose low
-// word carries for every row of a launch use hi + 1. Per site: one add, two
-// shift+LOP3 pairs, three IMADs (FMA pipe) and the sign test, where fin64_bit0
-// spends a 64-bit add, four shift+LOP3 pairs and five IMADs.
+// The same bit with fewer ALU-pipe instructions (the step kernel's
+// bottleneck). With lo, hi the words of z:
+//   lo32(z ^ z >> 30) = lo ^ (lo >> 30) ^ (hi << 2)
+//   hi32(z ^ z >> 30) = hi ^ (hi >> 30),
+// z1 = (z ^ z >> 30) * C1 is one IMAD.WIDE of the low word plus two IMADs
+// into its high word, and bit0(p) ^ bit31(p) of p = lo32(z1 ^ z1 >> 27) *
+// lo32(C2) is the sign bit of p * (1 + 2^31) = lo32(z1 ^ z1 >> 27) * kC2s.
+// `four` = 4, passed at run time, keeps hi << 2 an IMAD (FMA pipe).
 constexpr uint32_t kC2s = static_cast<uint32_t>(kC2) * 0x80000001u;
-FHPG_HD void chir_column(uint64_t key, uint32_t carry, uint32_t& lo, uint32_t& a, uint32_t& g) {
-  const uint32_t hi = static_cast<uint32_t>(key >> 32) + carry;
-  lo = static_cast<uint32_t>(key);
-  a = hi << 2;
-  g = (hi ^ (hi >> 30)) * static_cast<uint32_t>(kC1);
-}
-// Returns p * (1 + 2^31): its sign bit is the chirality bit.
-FHPG_HD int32_t chir_sign(uint32_t klo, uint32_t a, uint32_t g, uint32_t y) {
-  const uint32_t lo = klo + y;
-  const uint32_t zl = lo ^ (lo >> 30) ^ a;
+FHPG_HD uint32_t chir_bit(uint64_t z, uint32_t four) {
+  const uint32_t lo = static_cast<uint32_t>(z), hi = static_cast<uint32_t>(z >> 32);
+  const uint32_t zl = lo ^ (lo >> 30) ^ (hi * four);
+  const uint32_t g = (hi ^ (hi >> 30)) * static_cast<uint32_t>(kC1);
   const uint64_t w = static_cast<uint64_t>(zl) * static_cast<uint32_t>(kC1) +
                      (static_cast<uint64_t>(g) << 32);
   const uint32_t z1lo = static_cast<uint32_t>(w);
   const uint32_t z1hi = static_cast<uint32_t>(w >> 32) + zl * static_cast<uint32_t>(kC1 >> 32);
   const uint32_t lo2 = z1lo ^ ((z1lo >> 27) | (z1hi << 5));
-  return static_cast<int32_t>(lo2 * kC2s);
-}
-FHPG_HD bool chir_bit(uint32_t klo, uint32_t a, uint32_t g, uint32_t y) {
-  return chir_sign(klo, a, g, y) < 0;
+  return (lo2 * kC2s) >> 31;
 }
 
 // rng.hpp:37-42: bernoulli(word, p) == (word >> 32) < threshold(p).

@@ -40,8 +40,6 @@ struct StepArgs {
   int row_lo, row_hi;        // local row range to update, [row_lo, row_hi)
   int row_lo2 = 0, row_hi2 = 0;  // optional second range (bit-plane path: boundary rows)
   int segs1 = 0;             // row segments of the first range (bit-plane ring kernel)
-  int rng_exact = 0;         // test hook (FHPG_DEBUG_EXACT_RNG): ring kernel recomputes every
-                             // chirality bit from the 64-bit keys (its overflow path)
 };
 
 // Fast path launcher (fhpg_step_fast.cu).

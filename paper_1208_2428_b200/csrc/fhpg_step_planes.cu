@@ -106,13 +106,6 @@ __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint3
 __device__ __forceinline__ void red_or(uint32_t a, uint32_t v) {
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
 }
-// [a] |= v if q < 0. ptxas turns a predicated RED into a branch around it,
-// so the value is masked instead, on the FMA pipe (the ALU pipe is the
-// kernel's bottleneck): (q >> 31) = umulhi(q, two) with two = 2 passed at
-// run time (a literal 2 would be folded into a shift), times v.
-__device__ __forceinline__ void red_or_if(uint32_t a, uint32_t v, int32_t q, uint32_t two) {
-  red_or(a, __umulhi(static_cast<uint32_t>(q), two) * v);
-}
 __device__ __forceinline__ uint32_t top_bit(uint32_t m) {
   uint32_t p;
   asm("bfind.u32 %0, %1;" : "=r"(p) : "r"(m));
@@ -265,13 +258,11 @@ __device__ __forceinline__ void rd_shr(uint32_t a, uint32_t (&o)[NW]) {
 // split into 32 equal contiguous slices; each lane finds its first word
 // (binary search over the lanes' counts), skips the sites before its slice
 // and visits its sites, advancing through the list (it has no empty words).
-// fn(key address = word key address + j * KS) returns a value whose sign
-// bit is the site's result bit; set bits are ORed into the result words
-// (osm) by predicated shared-memory reductions.
-// Returns T.
-template <int NW, int KS, typename Fn>
+// fn(key address) returns the site's result bit, ORed into the result
+// words (osm). Returns T.
+template <int NW, typename Fn>
 __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint32_t osm,
-                                    uint32_t keys, int lane, uint32_t two, Fn&& fn) {
+                                    uint32_t keys, int lane, Fn&& fn) {
   int cnt = 0, nz = 0;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
@@ -294,8 +285,7 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
     for (int w = 0; w < NW; ++w) {
       if (m[w]) {
         const uint32_t wi = static_cast<uint32_t>(lane * NW + w);
-        sts128(lsm + q * 16, m[w], keys + wi * (32u * KS), static_cast<uint32_t>(c),
-               osm + wi * 4u);
+        sts128(lsm + q * 16, m[w], keys + wi * 256u, static_cast<uint32_t>(c), osm + wi * 4u);
         ++q;
         c += __popc(m[w]);
       }
@@ -316,7 +306,7 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
   const int o_excl = __shfl_sync(kFull, excl, o);
   if (s < e) {
     uint32_t qa = lsm + (o_excl >> 16) * 16u;  // list entry address
-    uint4 en = lds128(qa);                     // {mask left, key address, sites before, result word}
+    uint4 en = lds128(qa);
 #pragma unroll
     for (int w = 1; w < NW; ++w) {
       if (s >= static_cast<int>(en.z) + __popc(en.x)) {
@@ -324,49 +314,49 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
         en = lds128(qa);
       }
     }
-    // Sites are visited lowest bit first: skip the slice's predecessors.
-    for (int k = s - static_cast<int>(en.z); k > 0; --k) en.x &= en.x - 1u;
-    // Entry by entry; the last one keeps only the sites left in the slice
-    // (its highest bits are dropped).
-    int left = e - s;
-    for (;;) {
-      uint32_t mk = en.x;
-      const int c = __popc(mk);
-      if (c >= left) {
-        for (int d = c - left; d > 0; --d) mk ^= 1u << top_bit(mk);
-        left = 0;
-      } else {
-        left -= c;
+    // Sites are visited lowest bit first (measured a little faster than top
+    // bit first): skip the slice's predecessors.
+    uint32_t mask = en.x, kw = en.y, ow = en.w;
+    for (int k = s - static_cast<int>(en.z); k > 0; --k) mask &= mask - 1u;
+    // site: key address, result word address, bit index
+    auto next = [&](uint32_t& ka, uint32_t& wa, uint32_t& j) {
+      if (mask == 0u) {
+        qa += 16u;
+        const uint4 n = lds128(qa);
+        mask = n.x;
+        kw = n.y;
+        ow = n.w;
       }
-      const uint32_t kw = en.y, ow = en.w;
-      do {
-        // lowest set bit as a value (its product with the result bit stays
-        // an IMAD: ptxas cannot turn it into a shift) and as an index
-        const uint32_t bit = mk & (0u - mk);
-        mk ^= bit;
-        red_or_if(ow, bit, fn(kw + top_bit(bit) * KS), two);
-      } while (mk);
-      if (!left) break;
-      qa += 16u;
-      en = lds128(qa);
+      const uint32_t bit = mask & (0u - mask);
+      j = top_bit(bit);
+      mask ^= bit;
+      ka = kw + j * 8u;
+      wa = ow;
+    };
+    int it = s;
+    for (; it + 1 < e; it += 2) {
+      uint32_t k0, w0, j0, k1, w1, j1;
+      next(k0, w0, j0);
+      next(k1, w1, j1);
+      const uint32_t b0 = fn(k0), b1 = fn(k1);
+      red_or(w0, b0 << j0);
+      red_or(w1, b1 << j1);
+    }
+    if (it < e) {
+      uint32_t k0, w0, j0;
+      next(k0, w0, j0);
+      red_or(w0, fn(k0) << j0);
     }
   }
   __syncwarp();
   return T;
 }
 
-// Precomputed-column chirality keys of the ring kernel (chir_column): three
-// arrays of 4 B per band column, lo32(K) | A | G.
-constexpr int kMaxMix = 8;  // columns whose low key word starts carrying inside a CTA's rows
-
 template <int NW, bool FORCE>
 struct Ctx {
-  uint32_t kc;      // smem: chirality keys of the band (8 B per column; ring kernel: 3 x 4 B)
+  uint32_t kc;      // smem: chirality keys of the band (8 B per column)
   uint32_t kf;      // smem: forcing keys of the band (8 B per column)
-  const uint64_t* zg;  // ring kernel: the band's 64-bit chirality keys (global)
-  uint32_t mix;     // ring kernel: smem list of {band column, first carrying row}
-  int nmix;         // its length (> kMaxMix: recompute every chirality bit exactly)
-  uint32_t two;     // 2, passed at run time (red_or_if)
+  uint32_t four;    // 4, passed at run time (chir_bit)
   uint32_t lsm;     // smem: walk list
   uint32_t osm;     // smem: walk result words
   uint32_t stage;   // smem: output staging (the TMA store source)
@@ -377,7 +367,7 @@ struct Ctx {
 // of the slots of rows r-1, r, r+1; Q = global parity of r.
 // `released()` is called once the source rows have been read into
 // registers (the ring slots may be refilled from then on).
-template <int NW, bool FORCE, int Q, bool FASTKEY, typename Rel>
+template <int NW, bool FORCE, int Q, typename Rel>
 __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
                                          const Ctx<NW, FORCE>& cx, int lane, uint32_t y,
                                          const CUtensorMap* stmap, const CUtensorMap* padmap,
@@ -434,48 +424,9 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   __syncwarp();
   // Chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y)
   // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76).
-  int T;
-  if constexpr (FASTKEY) {
-    using G = Geo<NW, FORCE>;
-    constexpr uint32_t kA = G::kBandCols * 4, kG = 2 * G::kBandCols * 4;
-    T = walk<NW, 4>(dep, cx.lsm, cx.osm, cx.kc, lane, cx.two, [&](uint32_t ka) {
-      return chir_sign(lds32(ka), lds32(ka + kA), lds32(ka + kG), y);
-    });
-    if (T && cx.nmix) {
-      // Columns whose key's low word carries from some row of this CTA on
-      // (staged without the carry): recompute their bits exactly from the
-      // 64-bit keys. Practically never (the list is empty unless lo32(K)
-      // lies within a segment's row count of 2^32).
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const uint32_t wi = static_cast<uint32_t>(lane * NW + w);
-        uint32_t fm = 0u;
-        if (cx.nmix > kMaxMix) {
-          fm = ~0u;
-        } else {
-          for (int i = 0; i < cx.nmix; ++i) {
-            const uint2 me = lds64v(cx.mix + 8u + 8u * i);
-            if ((me.x >> 5) == wi && y >= me.y) fm |= 1u << (me.x & 31u);
-          }
-        }
-        uint32_t mm = dep[w] & fm;
-        if (mm) {
-          const uint32_t ra = cx.osm + wi * 4u;
-          uint32_t word = lds32(ra);
-          do {
-            const uint32_t j = top_bit(mm);
-            mm ^= 1u << j;
-            const uint32_t b = fin64_bit0(cx.zg[wi * 32u + j] + y);
-            word = (word & ~(1u << j)) | (b << j);
-          } while (mm);
-          sts32(ra, word);
-        }
-      }
-    }
-  } else {
-    T = walk<NW, 8>(dep, cx.lsm, cx.osm, cx.kc, lane, cx.two,
-                    [&](uint32_t ka) { return -static_cast<int32_t>(fin64_bit0(lds64(ka) + y)); });
-  }
+  // (chir_bit: fin64 bit 0 with fewer ALU-pipe instructions.)
+  const int T = walk<NW>(dep, cx.lsm, cx.osm, cx.kc, lane,
+                         [&](uint32_t ka) { return chir_bit(lds64(ka) + y, cx.four); });
   uint32_t o[NW][7];
   const uint32_t mine = cx.osm + lane * NW * 4;
 #pragma unroll
@@ -493,8 +444,8 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
     uint32_t f[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) f[w] = ~so[w] & o[w][5] & ~o[w][2];
-    const int TF = walk<NW, 8>(f, cx.lsm, cx.osm, cx.kf, lane, cx.two, [&](uint32_t ka) {
-      return (fin64(lds64(ka) + y) >> 32) < cx.thr ? -1 : 0;
+    const int TF = walk<NW>(f, cx.lsm, cx.osm, cx.kf, lane, [&](uint32_t ka) {
+      return (fin64(lds64(ka) + y) >> 32) < cx.thr ? 1u : 0u;
     });
     if (TF) {
 #pragma unroll
@@ -564,7 +515,7 @@ __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap
   auto one = [&](int r, auto qc) {
     constexpr int Q = decltype(qc)::value;
     wait(sn);
-    dest_row<NW, FORCE, Q, false>(ring + sm * G::kSlot + lane_off, ring + sc * G::kSlot + lane_off,
+    dest_row<NW, FORCE, Q>(ring + sm * G::kSlot + lane_off, ring + sc * G::kSlot + lane_off,
                            ring + sn * G::kSlot + lane_off, cx, L.lane, y0 + r, stmap, padmap,
                            L.w0, r + 1, L.pad, L.padx, L.pad_band, swaps, [] {});
     // The slot of row r-1 is free once every lane has read it.
@@ -653,10 +604,7 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
   cx.osm = osm;
   cx.stage = stage;
   cx.thr = a.thr;
-  cx.two = a.k2;
-  cx.zg = nullptr;
-  cx.mix = 0;
-  cx.nmix = 0;
+  cx.four = a.k4;
   unsigned swaps = 0;
   if ((a.row0 + r_begin) & 1)
     run_segment<NW, FORCE, 1>(a, &map, &stmap, &padmap, L, ring, bars, cx, r_begin, r_end, swaps);
@@ -681,6 +629,11 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 // ---------------------------------------------------------------------------
 // Consumer warps per CTA and ring slots (A/B on cfg4: 16/36 1570, 20/44
 // 1695, 24/52 1766, 30/64 1876, 31/48 1889 GSUPS).
+// Back-off of a consumer polling a slot's tag (ns): spinning warps take
+// issue slots from the working ones.
+#ifndef FHPG_TAG_SLEEP
+#define FHPG_TAG_SLEEP 64
+#endif
 #ifndef FHPG_RING_CONS
 #define FHPG_RING_CONS 31
 #endif
@@ -691,17 +644,15 @@ struct RingGeo {
 #ifdef FHPG_RING_SLOTS
   static constexpr int kRing = FHPG_RING_SLOTS;
 #else
-  static constexpr int kRing = FORCE ? 54 : 62;  // as many as the 227 KB allow
+  static constexpr int kRing = FORCE ? 56 : 64;  // as many as the 227 KB allow
 #endif
   static constexpr int kThreads = (kCons + 1) * 32;
-  // chirality: lo32(K) | A | G (4 B each per column); forcing: 64-bit keys
-  static constexpr int kKeys = G::kBandCols * 12 + (FORCE ? G::kBandCols * 8 : 0);
+  static constexpr int kKeys = (FORCE ? 2 : 1) * G::kBandCols * 8;
   static constexpr int kRingOff = (kKeys + 127) / 128 * 128;
   static constexpr int kStageOff = kRingOff + kRing * G::kSlot;
   static constexpr int kBarOff = kStageOff + kCons * G::kStageAll;
   static constexpr int kTagOff = kBarOff + 2 * 8 * kRing;
-  static constexpr int kMixOff = (kTagOff + 4 * kRing + 7) / 8 * 8;  // count, then kMaxMix x {col, row}
-  static constexpr int kSmem = kMixOff + 8 + 8 * kMaxMix;
+  static constexpr int kSmem = kTagOff + 4 * kRing;
   static_assert(kSmem <= 232448, "shared memory per CTA");
   static_assert(kRing % 2 == 0, "row pairs");
 };
@@ -730,7 +681,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   const int row_hi = second ? a.row_hi2 : a.row_hi;
   const int x0 = band * G::kBandCols;
   const uint32_t kc_base = sbase;
-  const uint32_t kf_base = sbase + G::kBandCols * 12;
+  const uint32_t kf_base = sbase + G::kBandCols * 8;
   const uint32_t ring = sbase + RG::kRingOff;
   const uint32_t full = sbase + RG::kBarOff;
   const uint32_t empty = full + 8 * RG::kRing;
@@ -739,10 +690,8 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   // mistake a slot two phases old for the one it needs; it first waits for
   // the tag, after which the full barrier's parity is unambiguous.
   const uint32_t tags = sbase + RG::kTagOff;
-  const uint32_t mix = sbase + RG::kMixOff;
   const int R0 = row_lo + seg_group * a.seg_rows;
   const int R1 = min(row_hi, R0 + a.seg_rows);
-  const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
   if (threadIdx.x == 0) {
     for (int k = 0; k < RG::kRing; ++k) {
       // Source rows come in pairs (one 2-row TMA box): pair P = index / 2
@@ -751,35 +700,11 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
       mbar_init(empty + k * 8, 6);
       sts32(tags + k * 4, 0xFFFFFFFFu);
     }
-    sts32(mix, 0u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  {
-    // Chirality keys with the column's share of fin64 precomputed
-    // (chir_column). A column whose low word carries for the CTA's first
-    // row is staged with the carry; one that starts carrying at a later row
-    // of the CTA goes to the mix list and is recomputed exactly from then on.
-    const uint32_t ylo = y0 + static_cast<uint32_t>(R0);
-    const uint32_t yhi = y0 + static_cast<uint32_t>(max(R1, R0 + 1) - 1);
-    for (int c = threadIdx.x; c < G::kBandCols; c += blockDim.x) {
-      const uint64_t K = a.zc[x0 + c];
-      const uint32_t klo = static_cast<uint32_t>(K);
-      const uint32_t carry = klo > ~ylo ? 1u : 0u;
-      uint32_t lo, A, Gk;
-      chir_column(K, carry, lo, A, Gk);
-      sts32(kc_base + c * 4, lo);
-      sts32(kc_base + G::kBandCols * 4 + c * 4, A);
-      sts32(kc_base + G::kBandCols * 8 + c * 4, Gk);
-      if (!carry && klo > ~yhi) {
-        uint32_t idx;
-        asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(idx) : "r"(mix) : "memory");
-        if (idx < kMaxMix)
-          asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(mix + 8u + 8u * idx),
-                       "r"(static_cast<uint32_t>(c)), "r"(0u - klo) : "memory");
-      }
-      if (FORCE) sts64(kf_base + c * 8, a.zf[x0 + c]);
-    }
+  for (int c = threadIdx.x; c < G::kBandCols; c += blockDim.x) {
+    sts64(kc_base + c * 8, a.zc[x0 + c]);
+    if (FORCE) sts64(kf_base + c * 8, a.zf[x0 + c]);
   }
   if (a.zc_next) {  // next step's column keys (read by the next launch only)
     const int n = gridDim.x * blockDim.x;
@@ -824,12 +749,10 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   cx.osm = stage + G::kList;
   cx.stage = stage;
   cx.thr = a.thr;
-  cx.two = a.k2;
-  cx.zg = a.zc + x0;
-  cx.mix = mix;
-  cx.nmix = a.rng_exact ? kMaxMix + 1 : static_cast<int>(lds32(mix));
+  cx.four = a.k4;
   unsigned swaps = 0;
   const uint32_t lane_off = 16u + lane * NW * 4u;
+  const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
   for (int r = R0 + warp; r < R1; r += RG::kCons) {
     const int i = r - R0;  // ring index of source row r - 1
     constexpr int kPairs = RG::kRing / 2;
@@ -843,7 +766,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
           uint32_t tag;
           asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tag) : "r"(tags + kp * 4) : "memory");
           if (tag == static_cast<uint32_t>(P)) break;
-          __nanosleep(64);
+          __nanosleep(FHPG_TAG_SLEEP);
         }
         mbar_wait(full + kp * 8, static_cast<uint32_t>((P / kPairs) & 1));
       }
@@ -862,10 +785,10 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
       }
     };
     if ((a.row0 + r) & 1)
-      dest_row<NW, FORCE, 1, true>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
+      dest_row<NW, FORCE, 1>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
                              L.pad, L.padx, L.pad_band, swaps, release);
     else
-      dest_row<NW, FORCE, 0, true>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
+      dest_row<NW, FORCE, 0>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
                              L.pad, L.padx, L.pad_band, swaps, release);
   }
   if (lane == 0) bulk_wait_all();  // the stores have landed before the kernel ends
@@ -881,7 +804,7 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
   using G = Geo<NW, FORCE>;
   using RG = RingGeo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
-  a.k2 = 2u;
+  a.k4 = 4u;
   a.nbands = a.W / G::kBandCols;
   int seg_groups = num_sms / a.nbands;
   if (seg_groups < 1) seg_groups = 1;
@@ -912,7 +835,7 @@ template <int NW, bool FORCE>
 void launch_nw(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st) {
   using G = Geo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
-  a.k2 = 2u;
+  a.k4 = 4u;
   a.nbands = a.W / G::kBandCols;
   // Bands per CTA: as many as the shared-memory budget allows (the column
   // keys of every band a CTA covers are staged).

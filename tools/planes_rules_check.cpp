@@ -73,9 +73,8 @@ int main() {
                [](const Fhp3Class& k, uint32_t c, uint32_t r, const uint32_t* x_a, uint32_t* o, uint32_t& orr) {
                  fhp3_apply(k, c, r, x_a, o, orr);
                });
-  // Precomputed-column chirality bit (fhpg_common.cuh chir_bit) == bit 0 of
-  // fin64(K + y) whenever lo32(K) + y does not carry, or carries with the
-  // carry folded into the column (random keys, keys at the carry boundary).
+  // chir_bit (fhpg_common.cuh) == bit 0 of fin64(z): random keys, and keys
+  // whose low word is at the carry boundary.
   {
     uint64_t st = 0x243F6A8885A308D3ull;
     long n = 0, wrong = 0;
@@ -83,15 +82,10 @@ int main() {
       st = mix64(st);
       uint64_t K = st;
       const uint32_t y = static_cast<uint32_t>(mix64(st ^ 1) >> 40);  // < 2^24
-      if (i % 4 == 1) K = (K & ~0xFFFFFFFFull) | (0xFFFFFFFFull - (y & 0xFF));  // at the boundary
+      if (i % 4 == 1) K = (K & ~0xFFFFFFFFull) | (0xFFFFFFFFull - (y & 0xFF));
       if (i % 4 == 2) K = (K & ~0xFFFFFFFFull) | (0x100000000ull - y + (st & 0xFF));
-      const uint32_t klo = static_cast<uint32_t>(K);
-      const uint32_t carry = static_cast<uint64_t>(klo) + y >= (1ull << 32) ? 1u : 0u;
-      uint32_t lo, a, g;
-      chir_column(K, carry, lo, a, g);
       ++n;
-      if ((chir_bit(lo, a, g, y) ? 1u : 0u) != (fin64_bit0(K + y) & 1u) ||
-          fin64_bit0(K + y) != (fin64(K + y) & 1u))
+      if (chir_bit(K + y, 4u) != (fin64(K + y) & 1u) || fin64_bit0(K + y) != (fin64(K + y) & 1u))
         ++wrong;
     }
     std::printf("chir_bit: %s (%ld keys)\n", wrong ? "MISMATCH" : "ok", n);
