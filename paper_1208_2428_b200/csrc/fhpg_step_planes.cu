@@ -56,8 +56,11 @@ namespace {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 // Warps per CTA (one CTA per SM): 16 with 2 words per lane, 8 with 4.
 #ifndef FHPG_STREAM_ONLY
-#define FHPG_STREAM_ONLY 0  // timing experiment: memory pipeline only (wrong results)
+#define FHPG_STREAM_ONLY 0  // timing experiments (wrong results): 1 memory pipeline only,
+                            // 2 loads only, 3 stores only, 4 loads + shared reads,
+                            // 5 compute + stores (no loads), 6 compute only
 #endif
+
 #ifndef FHPG_PLANES_RING
 #define FHPG_PLANES_RING 1
 #endif
@@ -149,6 +152,17 @@ __device__ __forceinline__ void bulk_commit() {
 }
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// Staging buffers per consumer warp (ring kernel): with 2 the TMA store of a
+// row may still be reading its buffer while the next row is computed.
+#ifndef FHPG_STAGE_BUFS
+#define FHPG_STAGE_BUFS 1
+#endif
+__device__ __forceinline__ void bulk_wait_read_stage() {
+  if (FHPG_STAGE_BUFS == 2)
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  else
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -319,7 +333,9 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
     uint32_t mask = en.x, kw = en.y, ow = en.w;
     for (int k = s - static_cast<int>(en.z); k > 0; --k) mask &= mask - 1u;
     // site: key address, result word address, bit index
-    auto next = [&](uint32_t& ka, uint32_t& wa, uint32_t& j) {
+    // j: bit index, v: 1 << j (the result bit's placement is an IMAD with
+    // v, FMA pipe, where a shift by j would take the ALU pipe)
+    auto next = [&](uint32_t& ka, uint32_t& wa, uint32_t& v) {
       if (mask == 0u) {
         qa += 16u;
         const uint4 n = lds128(qa);
@@ -327,41 +343,97 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
         kw = n.y;
         ow = n.w;
       }
-      const uint32_t bit = mask & (0u - mask);
-      j = top_bit(bit);
-      mask ^= bit;
-      ka = kw + j * 8u;
+      v = mask & (0u - mask);
+      mask ^= v;
+      ka = kw + top_bit(v) * 8u;
       wa = ow;
     };
     int it = s;
     for (; it + 1 < e; it += 2) {
-      uint32_t k0, w0, j0, k1, w1, j1;
-      next(k0, w0, j0);
-      next(k1, w1, j1);
+      uint32_t k0, w0, v0, k1, w1, v1;
+      next(k0, w0, v0);
+      next(k1, w1, v1);
       const uint32_t b0 = fn(k0), b1 = fn(k1);
-      red_or(w0, b0 << j0);
-      red_or(w1, b1 << j1);
+      red_or(w0, b0 * v0);
+      red_or(w1, b1 * v1);
     }
     if (it < e) {
-      uint32_t k0, w0, j0;
-      next(k0, w0, j0);
-      red_or(w0, fn(k0) << j0);
+      uint32_t k0, w0, v0;
+      next(k0, w0, v0);
+      red_or(w0, fn(k0) * v0);
     }
   }
   __syncwarp();
   return T;
 }
 
+// chir_bit (fhpg_common.cuh) with FHPG_HASH_FMA of its shifts moved to the
+// FMA pipe as IMAD / IMAD.HI by run-time powers of two (the ALU pipe is the
+// kernel's bottleneck): 1 = the two >> 30, 2 = also the funnel >> 27 / << 5,
+// 3 = also the final >> 31.
+#ifndef FHPG_HASH_FMA
+#define FHPG_HASH_FMA 0
+#endif
+__device__ __forceinline__ uint32_t chir_bit_dev(uint64_t z, uint32_t four, uint32_t k32) {
+  const uint32_t lo = static_cast<uint32_t>(z), hi = static_cast<uint32_t>(z >> 32);
+#if FHPG_HASH_FMA >= 1
+  const uint32_t zl = lo ^ __umulhi(lo, four) ^ (hi * four);
+  const uint32_t g = (hi ^ __umulhi(hi, four)) * static_cast<uint32_t>(kC1);
+#else
+  const uint32_t zl = lo ^ (lo >> 30) ^ (hi * four);
+  const uint32_t g = (hi ^ (hi >> 30)) * static_cast<uint32_t>(kC1);
+#endif
+  const uint64_t w = static_cast<uint64_t>(zl) * static_cast<uint32_t>(kC1) +
+                     (static_cast<uint64_t>(g) << 32);
+  const uint32_t z1lo = static_cast<uint32_t>(w);
+  const uint32_t z1hi = static_cast<uint32_t>(w >> 32) + zl * static_cast<uint32_t>(kC1 >> 32);
+#if FHPG_HASH_FMA >= 2
+  const uint32_t lo2 = z1lo ^ (z1hi * k32 + __umulhi(z1lo, k32));  // disjoint bits: + = |
+#else
+  const uint32_t lo2 = z1lo ^ __funnelshift_r(z1lo, z1hi, 27);
+#endif
+#if FHPG_HASH_FMA >= 3
+  return __umulhi(lo2 * kC2s, four >> 1);
+#else
+  return (lo2 * kC2s) >> 31;
+#endif
+}
+
 template <int NW, bool FORCE>
 struct Ctx {
   uint32_t kc;      // smem: chirality keys of the band (8 B per column)
   uint32_t kf;      // smem: forcing keys of the band (8 B per column)
-  uint32_t four;    // 4, passed at run time (chir_bit)
+  uint32_t four;    // 4, passed at run time (chir_bit_dev)
+  uint32_t k32;     // 32, passed at run time (chir_bit_dev)
   uint32_t lsm;     // smem: walk list
   uint32_t osm;     // smem: walk result words
   uint32_t stage;   // smem: output staging (the TMA store source)
+  uint8_t* gdst;    // FHPG_STG_STORES: destination local row 0
+  size_t pitch;
+  int WW;
   uint64_t thr;
 };
+
+// FHPG_STG_STORES = 1: the 7 outgoing plane words go straight from
+// registers to global memory (8-byte streaming stores, 256 B per plane and
+// warp), plus the periodic wrap copies; no staging, no TMA store.
+#ifndef FHPG_STG_STORES
+#define FHPG_STG_STORES 0
+#endif
+
+template <int NW, typename C>
+__device__ __forceinline__ void store_rows(const C& cx, int lane, int w0, int trow,
+                                           const uint32_t (&v)[7][NW]) {
+  const int wl = w0 + lane * NW;
+  const size_t prow = static_cast<size_t>(cx.WW + 8);  // padded plane row (words)
+  uint32_t* row = reinterpret_cast<uint32_t*>(cx.gdst + static_cast<size_t>(trow - 1) * cx.pitch);
+  const int padw = wl < 4 ? 4 + cx.WW + wl : (wl >= cx.WW - 4 ? wl - (cx.WW - 4) : -1);
+#pragma unroll
+  for (int p = 0; p < 7; ++p) {
+    stv<NW>(row + p * prow + 4 + wl, v[p]);
+    if (padw >= 0) stv<NW>(row + p * prow + padw, v[p]);
+  }
+}
 
 // One destination row. sm, sc, sn: this lane's word address inside plane 0
 // of the slots of rows r-1, r, r+1; Q = global parity of r.
@@ -387,10 +459,10 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   rd_al<NW>(sc + 6 * P, rr);
   rd_al<NW>(sc + 7 * P, so);
   released();
-#if FHPG_STREAM_ONLY
+#if FHPG_STREAM_ONLY && FHPG_STREAM_ONLY < 5
   // Timing experiment only (wrong results): the memory pipeline without the
   // collision and the chirality walk.
-  if (lane == 0) bulk_wait_read();
+  if (!FHPG_STG_STORES && lane == 0) bulk_wait_read();
   __syncwarp();
 #pragma unroll
   for (int p = 0; p < 7; ++p) {
@@ -401,12 +473,29 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
               : p == 5 ? a5[w] : rr[w]) ^ so[w];
     stsv<NW>(cx.stage + p * (4 * 32 * NW) + lane * NW * 4, v);
   }
+#if FHPG_STREAM_ONLY == 4  // timing experiment: loads + shared reads only
+  (void)swaps; (void)y; (void)pad; (void)padx; (void)pad_band; (void)padmap; (void)stmap;
+  return;
+#endif
+#if FHPG_STG_STORES
+  if (FHPG_STREAM_ONLY != 2) {
+    uint32_t v7[7][NW];
+#pragma unroll
+    for (int p = 0; p < 7; ++p)
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+        v7[p][w] = (p == 0 ? a0[w] : p == 1 ? a1[w] : p == 2 ? a2[w] : p == 3 ? a3[w] : p == 4 ? a4[w]
+                    : p == 5 ? a5[w] : rr[w]) ^ so[w];
+    store_rows<NW>(cx, lane, w0, trow, v7);
+  }
+#else
   fence_async_smem();
   __syncwarp();
-  if (lane == 0) {
+  if (lane == 0 && FHPG_STREAM_ONLY != 2) {  // 2: loads only
     tma_store(stmap, w0 + 4, trow, cx.stage);
     bulk_commit();
   }
+#endif
   (void)swaps; (void)y; (void)pad; (void)padx; (void)pad_band; (void)padmap;
   return;
 #endif
@@ -420,13 +509,13 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   }
   // The previous row's TMA store must have read the staging area (which
   // also holds the walk scratch) before it is rewritten.
-  if (lane == 0) bulk_wait_read();
+  if (!FHPG_STG_STORES && lane == 0) bulk_wait_read_stage();
   __syncwarp();
   // Chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y)
   // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76).
   // (chir_bit: fin64 bit 0 with fewer ALU-pipe instructions.)
   const int T = walk<NW>(dep, cx.lsm, cx.osm, cx.kc, lane,
-                         [&](uint32_t ka) { return chir_bit(lds64(ka) + y, cx.four); });
+                         [&](uint32_t ka) { return chir_bit_dev(lds64(ka) + y, cx.four, cx.k32); });
   uint32_t o[NW][7];
   const uint32_t mine = cx.osm + lane * NW * 4;
 #pragma unroll
@@ -457,6 +546,18 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
       }
     }
   }
+#if FHPG_STG_STORES
+  {
+    uint32_t v7[7][NW];
+#pragma unroll
+    for (int p = 0; p < 7; ++p)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) v7[p][w] = o[w][p];
+    store_rows<NW>(cx, lane, w0, trow, v7);
+    (void)pad; (void)padx; (void)pad_band; (void)padmap; (void)stmap;
+    return;
+  }
+#endif
 #pragma unroll
   for (int p = 0; p < 7; ++p) {
     uint32_t v[NW];
@@ -469,11 +570,13 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   fence_async_smem();
   __syncwarp();
   if (lane == 0) {
+#if FHPG_STREAM_ONLY != 6  // 6: no stores (timing experiment)
     tma_store(stmap, w0 + 4, trow, cx.stage);
     if (pad_band) {
       if (padx & 1) tma_store(padmap, 0, trow, cx.stage + Geo<NW, FORCE>::kPadL);
       if (padx & 2) tma_store(padmap, (padx >> 2) + 4, trow, cx.stage + Geo<NW, FORCE>::kPadR);
     }
+#endif
     bulk_commit();
   }
 }
@@ -605,6 +708,10 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
   cx.stage = stage;
   cx.thr = a.thr;
   cx.four = a.k4;
+  cx.k32 = a.k32;
+  cx.gdst = a.dst;
+  cx.pitch = a.pitch;
+  cx.WW = a.W >> 5;
   unsigned swaps = 0;
   if ((a.row0 + r_begin) & 1)
     run_segment<NW, FORCE, 1>(a, &map, &stmap, &padmap, L, ring, bars, cx, r_begin, r_end, swaps);
@@ -634,6 +741,12 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 #ifndef FHPG_TAG_SLEEP
 #define FHPG_TAG_SLEEP 64
 #endif
+// Source rows per TMA box: the producer warp's issue rate (one elected
+// thread: empty-barrier wait, tag, expect_tx, TMA per box) bounds the ring's
+// throughput, so each box carries several rows.
+#ifndef FHPG_BOX_ROWS
+#define FHPG_BOX_ROWS 4  // (2: 1972, 4: 1987-1995 GSUPS on cfg4)
+#endif
 #ifndef FHPG_RING_CONS
 #define FHPG_RING_CONS 31
 #endif
@@ -642,7 +755,7 @@ struct RingGeo {
   using G = Geo<NW, FORCE>;
   static constexpr int kCons = FHPG_RING_CONS;
 #ifdef FHPG_RING_SLOTS
-  static constexpr int kRing = FHPG_RING_SLOTS;
+  static constexpr int kRing = FORCE ? FHPG_RING_SLOTS_F : FHPG_RING_SLOTS;
 #else
   static constexpr int kRing = FORCE ? 56 : 64;  // as many as the 227 KB allow
 #endif
@@ -650,11 +763,13 @@ struct RingGeo {
   static constexpr int kKeys = (FORCE ? 2 : 1) * G::kBandCols * 8;
   static constexpr int kRingOff = (kKeys + 127) / 128 * 128;
   static constexpr int kStageOff = kRingOff + kRing * G::kSlot;
-  static constexpr int kBarOff = kStageOff + kCons * G::kStageAll;
+  static constexpr int kBarOff = kStageOff + FHPG_STAGE_BUFS * kCons * G::kStageAll;
   static constexpr int kTagOff = kBarOff + 2 * 8 * kRing;
   static constexpr int kSmem = kTagOff + 4 * kRing;
   static_assert(kSmem <= 232448, "shared memory per CTA");
-  static_assert(kRing % 2 == 0, "row pairs");
+  static constexpr int kBox = FHPG_BOX_ROWS;     // source rows per TMA box (a "group")
+  static constexpr int kGroups = kRing / kBox;   // ring slots of whole groups
+  static_assert(kRing % kBox == 0, "row groups");
 };
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar, uint32_t count) {
@@ -694,10 +809,10 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   const int R1 = min(row_hi, R0 + a.seg_rows);
   if (threadIdx.x == 0) {
     for (int k = 0; k < RG::kRing; ++k) {
-      // Source rows come in pairs (one 2-row TMA box): pair P = index / 2
-      // uses barriers / tag P mod kRing/2 (count 6 = 3 consumers per row).
+      // Source rows come in groups of kBox (one TMA box): group P = index /
+      // kBox uses barriers / tag P mod kGroups (3 consumers per row).
       mbar_init(full + k * 8, 1);
-      mbar_init(empty + k * 8, 6);
+      mbar_init(empty + k * 8, 3 * RG::kBox);
       sts32(tags + k * 4, 0xFFFFFFFFu);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -719,14 +834,23 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
 
   if (warp == RG::kCons) {  // producer: source rows R0-1 .. R1 (tensor row = local + 1)
     if (lane == 0) {
-      constexpr int kPairs = RG::kRing / 2;
-      const int npairs = (R1 - R0 + 3) / 2;  // rows R0-1 .. R1 (+ a spare zero row)
-      for (int P = 0; P < npairs; ++P) {
-        const int k = P % kPairs;
-        if (P >= kPairs) mbar_wait(empty + k * 8, static_cast<uint32_t>((P / kPairs - 1) & 1));
+      constexpr int kG = RG::kGroups, B = RG::kBox;
+      const int ngroups = (R1 - R0 + 1 + B) / B;  // rows R0-1 .. R1 (+ spare zero rows)
+      for (int P = 0; P < ngroups; ++P) {
+        const int k = P % kG;
+        if (P >= kG) mbar_wait(empty + k * 8, static_cast<uint32_t>((P / kG - 1) & 1));
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(tags + k * 4), "r"(P) : "memory");
-        mbar_expect_tx(full + k * 8, 2 * G::kRowBytes);
-        tma_row(ring + 2 * k * G::kSlot, &map2, w0, R0 + 2 * P, full + k * 8);  // tensor rows
+#if FHPG_STREAM_ONLY == 3 || FHPG_STREAM_ONLY >= 5  // timing experiments: no loads
+        if (FHPG_STREAM_ONLY >= 5 && P < kG) {  // 5, 6: compute on the first ring fill
+          mbar_expect_tx(full + k * 8, B * G::kRowBytes);
+          tma_row(ring + B * k * G::kSlot, &map2, w0, R0 + B * P, full + k * 8);
+        } else {
+          mbar_arrive(full + k * 8, 1);
+        }
+#else
+        mbar_expect_tx(full + k * 8, B * G::kRowBytes);
+        tma_row(ring + B * k * G::kSlot, &map2, w0, R0 + B * P, full + k * 8);  // tensor rows
+#endif
       }
     }
     return;
@@ -741,7 +865,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   L.pad = wl < 4 ? G::kPadR + wl * 4 : (wl >= L.WW - 4 ? G::kPadL + (wl - (L.WW - 4)) * 4 : -1);
   L.padx = (L.w0 + G::kBandWords == L.WW ? 1 : 0) | (L.w0 == 0 ? 2 : 0) | (L.WW << 2);
   L.pad_band = L.w0 == 0 || L.w0 + G::kBandWords == L.WW;
-  const uint32_t stage = sbase + RG::kStageOff + warp * G::kStageAll;
+  const uint32_t stage = sbase + RG::kStageOff + FHPG_STAGE_BUFS * warp * G::kStageAll;
   Ctx<NW, FORCE> cx;
   cx.kc = kc_base;
   cx.kf = kf_base;
@@ -750,25 +874,35 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   cx.stage = stage;
   cx.thr = a.thr;
   cx.four = a.k4;
+  cx.k32 = a.k32;
+  cx.gdst = a.dst;
+  cx.pitch = a.pitch;
+  cx.WW = a.W >> 5;
   unsigned swaps = 0;
   const uint32_t lane_off = 16u + lane * NW * 4u;
   const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
   for (int r = R0 + warp; r < R1; r += RG::kCons) {
     const int i = r - R0;  // ring index of source row r - 1
-    constexpr int kPairs = RG::kRing / 2;
+    constexpr int kG = RG::kGroups, B = RG::kBox;
+    if (FHPG_STAGE_BUFS == 2) {  // alternate staging buffers row by row
+      const uint32_t st = stage + ((i / RG::kCons) & 1) * G::kStageAll;
+      cx.lsm = st;
+      cx.osm = st + G::kList;
+      cx.stage = st;
+    }
     uint32_t sl[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      const int P = (i + d) >> 1;
-      if (d == 0 || ((i + d) & 1) == 0) {  // a new pair
-        const int kp = P % kPairs;
+      const int P = (i + d) / B;
+      if (d == 0 || ((i + d) % B) == 0) {  // a new group
+        const int kp = P % kG;
         for (;;) {
           uint32_t tag;
           asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tag) : "r"(tags + kp * 4) : "memory");
           if (tag == static_cast<uint32_t>(P)) break;
           __nanosleep(FHPG_TAG_SLEEP);
         }
-        mbar_wait(full + kp * 8, static_cast<uint32_t>((P / kPairs) & 1));
+        mbar_wait(full + kp * 8, static_cast<uint32_t>((P / kG) & 1));
       }
       sl[d] = ring + ((i + d) % RG::kRing) * G::kSlot + lane_off;
     }
@@ -779,9 +913,9 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         const uint32_t first = r == R0 ? 1u : 0u, lastr = r == R1 - 1 ? 1u : 0u;
-        mbar_arrive(empty + (((i) >> 1) % kPairs) * 8, 1 + 2 * first);
-        mbar_arrive(empty + (((i + 1) >> 1) % kPairs) * 8, 1 + first + lastr);
-        mbar_arrive(empty + (((i + 2) >> 1) % kPairs) * 8, 1 + 2 * lastr);
+        mbar_arrive(empty + ((i / B) % kG) * 8, 1 + 2 * first);
+        mbar_arrive(empty + (((i + 1) / B) % kG) * 8, 1 + first + lastr);
+        mbar_arrive(empty + (((i + 2) / B) % kG) * 8, 1 + 2 * lastr);
       }
     };
     if ((a.row0 + r) & 1)
@@ -805,6 +939,7 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
   using RG = RingGeo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
   a.k4 = 4u;
+  a.k32 = 32u;
   a.nbands = a.W / G::kBandCols;
   int seg_groups = num_sms / a.nbands;
   if (seg_groups < 1) seg_groups = 1;
@@ -836,6 +971,7 @@ void launch_nw(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st
   using G = Geo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
   a.k4 = 4u;
+  a.k32 = 32u;
   a.nbands = a.W / G::kBandCols;
   // Bands per CTA: as many as the shared-memory budget allows (the column
   // keys of every band a CTA covers are staged).
@@ -959,6 +1095,9 @@ bool planes_ok(int W) { return planes_words_per_lane(W) != 0; }
 
 size_t planes_row_bytes(int W) { return static_cast<size_t>(W) + 256; }
 
+#ifndef FHPG_L2PROMO
+#define FHPG_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows, int kind) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
@@ -980,11 +1119,21 @@ bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows,
                                  static_cast<cuuint64_t>(pitch)};
   const cuuint32_t box[3] = {
       static_cast<cuuint32_t>(kind == 0 || kind == 3 ? 32 * nw + 8 : kind == 1 ? 32 * nw : 4),
-      kind == 0 || kind == 3 ? 8u : 7u, kind == 3 ? 2u : 1u};
+      kind == 0 || kind == 3 ? 8u : 7u, kind == 3 ? static_cast<cuuint32_t>(FHPG_BOX_ROWS) : 1u};
   const cuuint32_t estr[3] = {1, 1, 1};
+#ifdef FHPG_EXP_CONTIG
+  // timing experiment: kind 3 reads 4 KB contiguous boxes
+  cuuint64_t xd[3] = {256, 2, static_cast<cuuint64_t>(pitch) * rows / 2048};
+  cuuint64_t xs[2] = {1024, 2048};
+  cuuint32_t xb[3] = {256, FHPG_EXP_CONTIG >= 2 ? 2u : 1u, FHPG_EXP_CONTIG >= 4 ? 2u : 1u};
+  const CUresult r = encode(static_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
+                            buffer, kind == 3 ? xd : dims, kind == 3 ? xs : strides,
+                            kind == 3 ? xb : box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+#else
   const CUresult r = encode(static_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
                             buffer, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+#endif
+                            CU_TENSOR_MAP_SWIZZLE_NONE, FHPG_L2PROMO,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
