@@ -747,6 +747,9 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 #ifndef FHPG_BOX_ROWS
 #define FHPG_BOX_ROWS 4  // (2: 1972, 4: 1987-1995 GSUPS on cfg4)
 #endif
+#ifndef FHPG_PDL
+#define FHPG_PDL 1
+#endif
 #ifndef FHPG_RING_CONS
 #define FHPG_RING_CONS 31
 #endif
@@ -817,6 +820,12 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+#if FHPG_PDL
+  // Let the next step's grid launch now; wait for the previous step's grid
+  // (its keys and lattice rows) before reading anything it wrote.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   for (int c = threadIdx.x; c < G::kBandCols; c += blockDim.x) {
     sts64(kc_base + c * 8, a.zc[x0 + c]);
     if (FORCE) sts64(kf_base + c * 8, a.zf[x0 + c]);
@@ -956,8 +965,25 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
                          RG::kSmem);
     attr = true;
   }
+#if FHPG_PDL
+  // Programmatic dependent launch: the next step's grid is launched while
+  // this one runs and its CTAs take SMs as they free up (griddepcontrol.wait
+  // in the kernel orders every read of the previous step's output).
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(RG::kThreads);
+  cfg.dynamicSmemBytes = RG::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, step_ring_kernel<NW, FORCE>, a, maps[0], maps[1], maps[2], maps[3]);
+#else
   step_ring_kernel<NW, FORCE><<<grid, RG::kThreads, RG::kSmem, st>>>(a, maps[0], maps[1], maps[2],
                                                                      maps[3]);
+#endif
 }
 
 template <int NW, bool FORCE>
