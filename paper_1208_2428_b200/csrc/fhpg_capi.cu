@@ -260,6 +260,8 @@ void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64
     a.table = e->table;
     a.zc = e->keys(s & 1, 0);
     a.zf = force ? e->keys(s & 1, 1) : nullptr;
+    a.kc_cur = step_key(seed, kChirality, s);
+    a.kf_cur = step_key(seed, kForcing, s);
     a.thr = thr;
     a.swaps = e->swaps;
     if (i + 1 < count) {
@@ -310,6 +312,8 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
   a.table = e->table;
   a.zc = e->keys(s & 1, 0);
   a.zf = force ? e->keys(s & 1, 1) : nullptr;
+  a.kc_cur = step_key(seed, kChirality, s);
+  a.kf_cur = step_key(seed, kForcing, s);
   a.thr = thr;
   a.swaps = e->swaps;
   const bool interior = e->nrows >= 3;

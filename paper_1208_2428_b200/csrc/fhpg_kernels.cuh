@@ -29,6 +29,7 @@ struct StepArgs {
   uint64_t* zc_next;         // column keys of the next step (may be null)
   uint64_t* zf_next;
   uint64_t kc_next, kf_next; // step keys of the next step
+  uint64_t kc_cur, kf_cur;   // step keys of this step (ring kernel: column keys made in-kernel)
   // Powers of two passed at run time so that ptxas keeps the byte moves that
   // use them as IMAD / IMAD.HI (FMA pipe) instead of folding them into
   // shifts on the ALU pipe, which the fast path saturates (fast path only).

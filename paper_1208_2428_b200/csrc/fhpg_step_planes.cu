@@ -820,16 +820,18 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // The band's column keys, made here from the step keys (they depend on
+  // nothing the previous step wrote, so this overlaps its tail under PDL).
+  for (int c = threadIdx.x; c < G::kBandCols; c += blockDim.x) {
+    sts64(kc_base + c * 8, column_key(a.kc_cur, static_cast<uint64_t>(x0 + c) + 1));
+    if (FORCE) sts64(kf_base + c * 8, column_key(a.kf_cur, static_cast<uint64_t>(x0 + c) + 1));
+  }
 #if FHPG_PDL
   // Let the next step's grid launch now; wait for the previous step's grid
-  // (its keys and lattice rows) before reading anything it wrote.
+  // (the lattice rows it wrote, the key buffers it read) before going on.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
-  for (int c = threadIdx.x; c < G::kBandCols; c += blockDim.x) {
-    sts64(kc_base + c * 8, a.zc[x0 + c]);
-    if (FORCE) sts64(kf_base + c * 8, a.zf[x0 + c]);
-  }
   if (a.zc_next) {  // next step's column keys (read by the next launch only)
     const int n = gridDim.x * blockDim.x;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.W; i += n) {
