@@ -893,8 +893,8 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   const uint32_t lane_off = 16u + lane * NW * 4u;
   const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
   for (int r = R0 + warp; r < R1; r += RG::kCons) {
-    const int i = r - R0;  // ring index of source row r - 1
-    constexpr int kG = RG::kGroups, B = RG::kBox;
+    const uint32_t i = static_cast<uint32_t>(r - R0);  // ring index of source row r - 1
+    constexpr uint32_t kG = RG::kGroups, B = RG::kBox;
     if (FHPG_STAGE_BUFS == 2) {  // alternate staging buffers row by row
       const uint32_t st = stage + ((i / RG::kCons) & 1) * G::kStageAll;
       cx.lsm = st;
@@ -903,30 +903,35 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
     }
     uint32_t sl[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const int P = (i + d) / B;
+    for (uint32_t d = 0; d < 3; ++d) {
+      const uint32_t P = (i + d) / B;
       if (d == 0 || ((i + d) % B) == 0) {  // a new group
-        const int kp = P % kG;
+        const uint32_t kp = P % kG;
         for (;;) {
           uint32_t tag;
           asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tag) : "r"(tags + kp * 4) : "memory");
-          if (tag == static_cast<uint32_t>(P)) break;
+          if (tag == P) break;
           __nanosleep(FHPG_TAG_SLEEP);
         }
-        mbar_wait(full + kp * 8, static_cast<uint32_t>((P / kG) & 1));
+        mbar_wait(full + kp * 8, (P / kG) & 1u);
       }
       sl[d] = ring + ((i + d) % RG::kRing) * G::kSlot + lane_off;
     }
     // Release the three source rows as soon as they are in registers (3
     // consumers per row; segment edges make up for the destination rows
-    // outside [R0, R1)).
+    // outside [R0, R1)); one arrive per group the rows fall in.
     auto release = [&] {
       __syncwarp();
       if (lane == 0) {
         const uint32_t first = r == R0 ? 1u : 0u, lastr = r == R1 - 1 ? 1u : 0u;
-        mbar_arrive(empty + ((i / B) % kG) * 8, 1 + 2 * first);
-        mbar_arrive(empty + (((i + 1) / B) % kG) * 8, 1 + first + lastr);
-        mbar_arrive(empty + (((i + 2) / B) % kG) * 8, 1 + 2 * lastr);
+        const uint32_t c0 = 1 + 2 * first, c1 = 1 + first + lastr, c2 = 1 + 2 * lastr;
+        const uint32_t g0 = i / B, g1 = (i + 1) / B, g2 = (i + 2) / B;
+        if (g0 == g2) {
+          mbar_arrive(empty + (g0 % kG) * 8, c0 + c1 + c2);
+        } else {
+          mbar_arrive(empty + (g0 % kG) * 8, c0 + (g1 == g0 ? c1 : 0u));
+          mbar_arrive(empty + (g2 % kG) * 8, c2 + (g1 == g2 ? c1 : 0u));
+        }
       }
     };
     if ((a.row0 + r) & 1)
