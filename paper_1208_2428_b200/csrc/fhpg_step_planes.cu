@@ -153,17 +153,7 @@ __device__ __forceinline__ void bulk_commit() {
 __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
-// Staging buffers per consumer warp (ring kernel): with 2 the TMA store of a
-// row may still be reading its buffer while the next row is computed.
-#ifndef FHPG_STAGE_BUFS
-#define FHPG_STAGE_BUFS 1
-#endif
-__device__ __forceinline__ void bulk_wait_read_stage() {
-  if (FHPG_STAGE_BUFS == 2)
-    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-  else
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
+
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
@@ -367,73 +357,16 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
   return T;
 }
 
-// chir_bit (fhpg_common.cuh) with FHPG_HASH_FMA of its shifts moved to the
-// FMA pipe as IMAD / IMAD.HI by run-time powers of two (the ALU pipe is the
-// kernel's bottleneck): 1 = the two >> 30, 2 = also the funnel >> 27 / << 5,
-// 3 = also the final >> 31.
-#ifndef FHPG_HASH_FMA
-#define FHPG_HASH_FMA 0
-#endif
-__device__ __forceinline__ uint32_t chir_bit_dev(uint64_t z, uint32_t four, uint32_t k32) {
-  const uint32_t lo = static_cast<uint32_t>(z), hi = static_cast<uint32_t>(z >> 32);
-#if FHPG_HASH_FMA >= 1
-  const uint32_t zl = lo ^ __umulhi(lo, four) ^ (hi * four);
-  const uint32_t g = (hi ^ __umulhi(hi, four)) * static_cast<uint32_t>(kC1);
-#else
-  const uint32_t zl = lo ^ (lo >> 30) ^ (hi * four);
-  const uint32_t g = (hi ^ (hi >> 30)) * static_cast<uint32_t>(kC1);
-#endif
-  const uint64_t w = static_cast<uint64_t>(zl) * static_cast<uint32_t>(kC1) +
-                     (static_cast<uint64_t>(g) << 32);
-  const uint32_t z1lo = static_cast<uint32_t>(w);
-  const uint32_t z1hi = static_cast<uint32_t>(w >> 32) + zl * static_cast<uint32_t>(kC1 >> 32);
-#if FHPG_HASH_FMA >= 2
-  const uint32_t lo2 = z1lo ^ (z1hi * k32 + __umulhi(z1lo, k32));  // disjoint bits: + = |
-#else
-  const uint32_t lo2 = z1lo ^ __funnelshift_r(z1lo, z1hi, 27);
-#endif
-#if FHPG_HASH_FMA >= 3
-  return __umulhi(lo2 * kC2s, four >> 1);
-#else
-  return (lo2 * kC2s) >> 31;
-#endif
-}
-
 template <int NW, bool FORCE>
 struct Ctx {
   uint32_t kc;      // smem: chirality keys of the band (8 B per column)
   uint32_t kf;      // smem: forcing keys of the band (8 B per column)
-  uint32_t four;    // 4, passed at run time (chir_bit_dev)
-  uint32_t k32;     // 32, passed at run time (chir_bit_dev)
+  uint32_t four;    // 4, passed at run time (chir_bit)
   uint32_t lsm;     // smem: walk list
   uint32_t osm;     // smem: walk result words
   uint32_t stage;   // smem: output staging (the TMA store source)
-  uint8_t* gdst;    // FHPG_STG_STORES: destination local row 0
-  size_t pitch;
-  int WW;
   uint64_t thr;
 };
-
-// FHPG_STG_STORES = 1: the 7 outgoing plane words go straight from
-// registers to global memory (8-byte streaming stores, 256 B per plane and
-// warp), plus the periodic wrap copies; no staging, no TMA store.
-#ifndef FHPG_STG_STORES
-#define FHPG_STG_STORES 0
-#endif
-
-template <int NW, typename C>
-__device__ __forceinline__ void store_rows(const C& cx, int lane, int w0, int trow,
-                                           const uint32_t (&v)[7][NW]) {
-  const int wl = w0 + lane * NW;
-  const size_t prow = static_cast<size_t>(cx.WW + 8);  // padded plane row (words)
-  uint32_t* row = reinterpret_cast<uint32_t*>(cx.gdst + static_cast<size_t>(trow - 1) * cx.pitch);
-  const int padw = wl < 4 ? 4 + cx.WW + wl : (wl >= cx.WW - 4 ? wl - (cx.WW - 4) : -1);
-#pragma unroll
-  for (int p = 0; p < 7; ++p) {
-    stv<NW>(row + p * prow + 4 + wl, v[p]);
-    if (padw >= 0) stv<NW>(row + p * prow + padw, v[p]);
-  }
-}
 
 // One destination row. sm, sc, sn: this lane's word address inside plane 0
 // of the slots of rows r-1, r, r+1; Q = global parity of r.
@@ -462,7 +395,7 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
 #if FHPG_STREAM_ONLY && FHPG_STREAM_ONLY < 5
   // Timing experiment only (wrong results): the memory pipeline without the
   // collision and the chirality walk.
-  if (!FHPG_STG_STORES && lane == 0) bulk_wait_read();
+  if (lane == 0) bulk_wait_read();
   __syncwarp();
 #pragma unroll
   for (int p = 0; p < 7; ++p) {
@@ -477,25 +410,12 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   (void)swaps; (void)y; (void)pad; (void)padx; (void)pad_band; (void)padmap; (void)stmap;
   return;
 #endif
-#if FHPG_STG_STORES
-  if (FHPG_STREAM_ONLY != 2) {
-    uint32_t v7[7][NW];
-#pragma unroll
-    for (int p = 0; p < 7; ++p)
-#pragma unroll
-      for (int w = 0; w < NW; ++w)
-        v7[p][w] = (p == 0 ? a0[w] : p == 1 ? a1[w] : p == 2 ? a2[w] : p == 3 ? a3[w] : p == 4 ? a4[w]
-                    : p == 5 ? a5[w] : rr[w]) ^ so[w];
-    store_rows<NW>(cx, lane, w0, trow, v7);
-  }
-#else
   fence_async_smem();
   __syncwarp();
   if (lane == 0 && FHPG_STREAM_ONLY != 2) {  // 2: loads only
     tma_store(stmap, w0 + 4, trow, cx.stage);
     bulk_commit();
   }
-#endif
   (void)swaps; (void)y; (void)pad; (void)padx; (void)pad_band; (void)padmap;
   return;
 #endif
@@ -509,13 +429,13 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   }
   // The previous row's TMA store must have read the staging area (which
   // also holds the walk scratch) before it is rewritten.
-  if (!FHPG_STG_STORES && lane == 0) bulk_wait_read_stage();
+  if (lane == 0) bulk_wait_read();
   __syncwarp();
   // Chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y)
   // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76).
   // (chir_bit: fin64 bit 0 with fewer ALU-pipe instructions.)
   const int T = walk<NW>(dep, cx.lsm, cx.osm, cx.kc, lane,
-                         [&](uint32_t ka) { return chir_bit_dev(lds64(ka) + y, cx.four, cx.k32); });
+                         [&](uint32_t ka) { return chir_bit(lds64(ka) + y, cx.four); });
   uint32_t o[NW][7];
   const uint32_t mine = cx.osm + lane * NW * 4;
 #pragma unroll
@@ -546,18 +466,6 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
       }
     }
   }
-#if FHPG_STG_STORES
-  {
-    uint32_t v7[7][NW];
-#pragma unroll
-    for (int p = 0; p < 7; ++p)
-#pragma unroll
-      for (int w = 0; w < NW; ++w) v7[p][w] = o[w][p];
-    store_rows<NW>(cx, lane, w0, trow, v7);
-    (void)pad; (void)padx; (void)pad_band; (void)padmap; (void)stmap;
-    return;
-  }
-#endif
 #pragma unroll
   for (int p = 0; p < 7; ++p) {
     uint32_t v[NW];
@@ -708,10 +616,6 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
   cx.stage = stage;
   cx.thr = a.thr;
   cx.four = a.k4;
-  cx.k32 = a.k32;
-  cx.gdst = a.dst;
-  cx.pitch = a.pitch;
-  cx.WW = a.W >> 5;
   unsigned swaps = 0;
   if ((a.row0 + r_begin) & 1)
     run_segment<NW, FORCE, 1>(a, &map, &stmap, &padmap, L, ring, bars, cx, r_begin, r_end, swaps);
@@ -766,7 +670,7 @@ struct RingGeo {
   static constexpr int kKeys = (FORCE ? 2 : 1) * G::kBandCols * 8;
   static constexpr int kRingOff = (kKeys + 127) / 128 * 128;
   static constexpr int kStageOff = kRingOff + kRing * G::kSlot;
-  static constexpr int kBarOff = kStageOff + FHPG_STAGE_BUFS * kCons * G::kStageAll;
+  static constexpr int kBarOff = kStageOff + kCons * G::kStageAll;
   static constexpr int kTagOff = kBarOff + 2 * 8 * kRing;
   static constexpr int kSmem = kTagOff + 4 * kRing;
   static_assert(kSmem <= 232448, "shared memory per CTA");
@@ -876,7 +780,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   L.pad = wl < 4 ? G::kPadR + wl * 4 : (wl >= L.WW - 4 ? G::kPadL + (wl - (L.WW - 4)) * 4 : -1);
   L.padx = (L.w0 + G::kBandWords == L.WW ? 1 : 0) | (L.w0 == 0 ? 2 : 0) | (L.WW << 2);
   L.pad_band = L.w0 == 0 || L.w0 + G::kBandWords == L.WW;
-  const uint32_t stage = sbase + RG::kStageOff + FHPG_STAGE_BUFS * warp * G::kStageAll;
+  const uint32_t stage = sbase + RG::kStageOff + warp * G::kStageAll;
   Ctx<NW, FORCE> cx;
   cx.kc = kc_base;
   cx.kf = kf_base;
@@ -885,22 +789,12 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   cx.stage = stage;
   cx.thr = a.thr;
   cx.four = a.k4;
-  cx.k32 = a.k32;
-  cx.gdst = a.dst;
-  cx.pitch = a.pitch;
-  cx.WW = a.W >> 5;
   unsigned swaps = 0;
   const uint32_t lane_off = 16u + lane * NW * 4u;
   const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
   for (int r = R0 + warp; r < R1; r += RG::kCons) {
     const uint32_t i = static_cast<uint32_t>(r - R0);  // ring index of source row r - 1
     constexpr uint32_t kG = RG::kGroups, B = RG::kBox;
-    if (FHPG_STAGE_BUFS == 2) {  // alternate staging buffers row by row
-      const uint32_t st = stage + ((i / RG::kCons) & 1) * G::kStageAll;
-      cx.lsm = st;
-      cx.osm = st + G::kList;
-      cx.stage = st;
-    }
     uint32_t sl[3];
 #pragma unroll
     for (uint32_t d = 0; d < 3; ++d) {
@@ -955,7 +849,6 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
   using RG = RingGeo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
   a.k4 = 4u;
-  a.k32 = 32u;
   a.nbands = a.W / G::kBandCols;
   int seg_groups = num_sms / a.nbands;
   if (seg_groups < 1) seg_groups = 1;
@@ -1004,7 +897,6 @@ void launch_nw(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st
   using G = Geo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
   a.k4 = 4u;
-  a.k32 = 32u;
   a.nbands = a.W / G::kBandCols;
   // Bands per CTA: as many as the shared-memory budget allows (the column
   // keys of every band a CTA covers are staged).
@@ -1128,9 +1020,6 @@ bool planes_ok(int W) { return planes_words_per_lane(W) != 0; }
 
 size_t planes_row_bytes(int W) { return static_cast<size_t>(W) + 256; }
 
-#ifndef FHPG_L2PROMO
-#define FHPG_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-#endif
 bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows, int kind) {
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
@@ -1154,19 +1043,9 @@ bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows,
       static_cast<cuuint32_t>(kind == 0 || kind == 3 ? 32 * nw + 8 : kind == 1 ? 32 * nw : 4),
       kind == 0 || kind == 3 ? 8u : 7u, kind == 3 ? static_cast<cuuint32_t>(FHPG_BOX_ROWS) : 1u};
   const cuuint32_t estr[3] = {1, 1, 1};
-#ifdef FHPG_EXP_CONTIG
-  // timing experiment: kind 3 reads 4 KB contiguous boxes
-  cuuint64_t xd[3] = {256, 2, static_cast<cuuint64_t>(pitch) * rows / 2048};
-  cuuint64_t xs[2] = {1024, 2048};
-  cuuint32_t xb[3] = {256, FHPG_EXP_CONTIG >= 2 ? 2u : 1u, FHPG_EXP_CONTIG >= 4 ? 2u : 1u};
-  const CUresult r = encode(static_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
-                            buffer, kind == 3 ? xd : dims, kind == 3 ? xs : strides,
-                            kind == 3 ? xb : box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-#else
   const CUresult r = encode(static_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
                             buffer, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-#endif
-                            CU_TENSOR_MAP_SWIZZLE_NONE, FHPG_L2PROMO,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
