@@ -754,7 +754,10 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
       for (int P = 0; P < ngroups; ++P) {
         const int k = P % kG;
         if (P >= kG) mbar_wait(empty + k * 8, static_cast<uint32_t>((P / kG - 1) & 1));
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(tags + k * 4), "r"(P) : "memory");
+        {  // tag: an atomic store (consumers poll it; not a data race)
+          uint32_t prev;
+          asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(prev) : "r"(tags + k * 4), "r"(P) : "memory");
+        }
 #if FHPG_STREAM_ONLY == 3 || FHPG_STREAM_ONLY >= 5  // timing experiments: no loads
         if (FHPG_STREAM_ONLY >= 5 && P < kG) {  // 5, 6: compute on the first ring fill
           mbar_expect_tx(full + k * 8, B * G::kRowBytes);
@@ -803,7 +806,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
         const uint32_t kp = P % kG;
         for (;;) {
           uint32_t tag;
-          asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(tag) : "r"(tags + kp * 4) : "memory");
+          asm volatile("ld.relaxed.cta.shared.u32 %0, [%1];" : "=r"(tag) : "r"(tags + kp * 4) : "memory");
           if (tag == P) break;
           __nanosleep(FHPG_TAG_SLEEP);
         }
