@@ -41,6 +41,8 @@ struct StepArgs {
   int row_lo, row_hi;        // local row range to update, [row_lo, row_hi)
   int row_lo2 = 0, row_hi2 = 0;  // optional second range (bit-plane path: boundary rows)
   int segs1 = 0;             // row segments of the first range (bit-plane ring kernel)
+  int segs2 = 0;             //   ... of the second range
+  int extra_rows = 0;        // ring kernel: last rows of every band done by the extra CTAs
 };
 
 // Fast path launcher (fhpg_step_fast.cu).

@@ -654,6 +654,12 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 #ifndef FHPG_PDL
 #define FHPG_PDL 1
 #endif
+#ifndef FHPG_EXTRA_CTAS
+#define FHPG_EXTRA_CTAS 1
+#endif
+#ifndef FHPG_EXTRA_BUBBLE_ROWS
+#define FHPG_EXTRA_BUBBLE_ROWS 20
+#endif
 #ifndef FHPG_RING_CONS
 #define FHPG_RING_CONS 31
 #endif
@@ -695,13 +701,35 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int band = blockIdx.x % a.nbands;
-  // Segments of the first row range, then of the optional second one.
-  const bool second = static_cast<int>(blockIdx.x / a.nbands) >= a.segs1;
-  const int seg_group = blockIdx.x / a.nbands - (second ? a.segs1 : 0);
-  const int row_lo = second ? a.row_lo2 : a.row_lo;
-  const int row_hi = second ? a.row_hi2 : a.row_hi;
-  const int x0 = band * G::kBandCols;
+  // Work of this CTA: part A = band bA, rows [RA0, RA0 + nA), and for the
+  // extra CTAs (the SMs left over by nbands x segment groups) part B = band
+  // bA + 1 over the same rows. Main CTAs: a band x a segment of one of the
+  // row ranges (the second range: a strip's boundary rows); with extra CTAs
+  // the first range's last extra_rows rows of every band go to them, the
+  // bands still walking the same rows at the same time (adjacent bands share
+  // the sectors at their edges in L2).
+  const int nmain = a.nbands * (a.segs1 + a.segs2);
+  int bA, RA0, nA, nB = 0;
+  int row_lo;
+  if (static_cast<int>(blockIdx.x) < nmain) {
+    bA = blockIdx.x % a.nbands;
+    const bool second = static_cast<int>(blockIdx.x / a.nbands) >= a.segs1;
+    const int seg_group = blockIdx.x / a.nbands - (second ? a.segs1 : 0);
+    row_lo = second ? a.row_lo2 : a.row_lo;
+    const int row_hi = second ? a.row_hi2 : a.row_hi - a.extra_rows;
+    RA0 = row_lo + seg_group * a.seg_rows;
+    nA = max(0, min(row_hi, RA0 + a.seg_rows) - RA0);
+  } else {
+    bA = 2 * (blockIdx.x - nmain);
+    row_lo = a.row_hi - a.extra_rows;
+    RA0 = row_lo;
+    nA = a.extra_rows;
+    nB = bA + 1 < a.nbands ? a.extra_rows : 0;
+  }
+  constexpr uint32_t B = RG::kBox;
+  // Ring index layout: part A's source rows RA0-1 .. RA0+nA, then part B's
+  // (row_lo-1 .. row_lo+nB) from the next whole group on.
+  const uint32_t offB = (static_cast<uint32_t>(nA) + 2 + B - 1) / B * B;
   const uint32_t kc_base = sbase;
   const uint32_t kf_base = sbase + G::kBandCols * 8;
   const uint32_t ring = sbase + RG::kRingOff;
@@ -712,8 +740,6 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   // mistake a slot two phases old for the one it needs; it first waits for
   // the tag, after which the full barrier's parity is unambiguous.
   const uint32_t tags = sbase + RG::kTagOff;
-  const int R0 = row_lo + seg_group * a.seg_rows;
-  const int R1 = min(row_hi, R0 + a.seg_rows);
   if (threadIdx.x == 0) {
     for (int k = 0; k < RG::kRing; ++k) {
       // Source rows come in groups of kBox (one TMA box): group P = index /
@@ -726,10 +752,14 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   }
   // The band's column keys, made here from the step keys (they depend on
   // nothing the previous step wrote, so this overlaps its tail under PDL).
-  for (int c = threadIdx.x; c < G::kBandCols; c += blockDim.x) {
-    sts64(kc_base + c * 8, column_key(a.kc_cur, static_cast<uint64_t>(x0 + c) + 1));
-    if (FORCE) sts64(kf_base + c * 8, column_key(a.kf_cur, static_cast<uint64_t>(x0 + c) + 1));
-  }
+  auto make_keys = [&](int b, int t0, int nt) {
+    for (int c = t0; c < G::kBandCols; c += nt) {
+      const uint64_t x = static_cast<uint64_t>(b * G::kBandCols + c) + 1;
+      sts64(kc_base + c * 8, column_key(a.kc_cur, x));
+      if (FORCE) sts64(kf_base + c * 8, column_key(a.kf_cur, x));
+    }
+  };
+  make_keys(bA, threadIdx.x, blockDim.x);
 #if FHPG_PDL
   // Let the next step's grid launch now; wait for the previous step's grid
   // (the lattice rows it wrote, the key buffers it read) before going on.
@@ -744,31 +774,39 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
     }
   }
   __syncthreads();
-  if (R0 >= R1) return;
-  const int w0 = band * G::kBandWords;
+  if (nA + nB <= 0) return;
 
-  if (warp == RG::kCons) {  // producer: source rows R0-1 .. R1 (tensor row = local + 1)
+  if (warp == RG::kCons) {  // producer (tensor row = local row + 1)
     if (lane == 0) {
-      constexpr int kG = RG::kGroups, B = RG::kBox;
-      const int ngroups = (R1 - R0 + 1 + B) / B;  // rows R0-1 .. R1 (+ spare zero rows)
-      for (int P = 0; P < ngroups; ++P) {
-        const int k = P % kG;
-        if (P >= kG) mbar_wait(empty + k * 8, static_cast<uint32_t>((P / kG - 1) & 1));
+      constexpr uint32_t kG = RG::kGroups;
+      const uint32_t gA = offB / B;
+      const uint32_t ngroups = gA + (nB > 0 ? (static_cast<uint32_t>(nB) + 2 + B - 1) / B : 0u);
+      for (uint32_t P = 0; P < ngroups; ++P) {
+        const uint32_t k = P % kG;
+        if (P >= kG) mbar_wait(empty + k * 8, (P / kG - 1) & 1u);
         {  // tag: an atomic store (consumers poll it; not a data race)
           uint32_t prev;
           asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(prev) : "r"(tags + k * 4), "r"(P) : "memory");
         }
+        const bool inA = P < gA;
+        const int word = (inA ? bA : bA + 1) * G::kBandWords;
+        const int trow = inA ? RA0 + static_cast<int>(B * P) : row_lo + static_cast<int>(B * P - offB);
 #if FHPG_STREAM_ONLY == 3 || FHPG_STREAM_ONLY >= 5  // timing experiments: no loads
         if (FHPG_STREAM_ONLY >= 5 && P < kG) {  // 5, 6: compute on the first ring fill
           mbar_expect_tx(full + k * 8, B * G::kRowBytes);
-          tma_row(ring + B * k * G::kSlot, &map2, w0, R0 + B * P, full + k * 8);
+          tma_row(ring + B * k * G::kSlot, &map2, word, trow, full + k * 8);
         } else {
           mbar_arrive(full + k * 8, 1);
         }
 #else
         mbar_expect_tx(full + k * 8, B * G::kRowBytes);
-        tma_row(ring + B * k * G::kSlot, &map2, w0, R0 + B * P, full + k * 8);  // tensor rows
+        tma_row(ring + B * k * G::kSlot, &map2, word, trow, full + k * 8);  // tensor rows
 #endif
+        // Ring indices no destination row reads (the tail of part A's last
+        // group when part B follows) still count 3 arrivals each, or the
+        // slot is never freed.
+        if (nB > 0 && P + 1 == gA && offB > static_cast<uint32_t>(nA) + 2)
+          mbar_arrive(empty + k * 8, 3 * (offB - static_cast<uint32_t>(nA) - 2));
       }
     }
     return;
@@ -778,11 +816,14 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   L.lane = lane;
   L.WW = a.W >> 5;
   L.PW = L.WW + 8;
-  L.w0 = w0;
-  const int wl = L.w0 + L.lane * NW;
-  L.pad = wl < 4 ? G::kPadR + wl * 4 : (wl >= L.WW - 4 ? G::kPadL + (wl - (L.WW - 4)) * 4 : -1);
-  L.padx = (L.w0 + G::kBandWords == L.WW ? 1 : 0) | (L.w0 == 0 ? 2 : 0) | (L.WW << 2);
-  L.pad_band = L.w0 == 0 || L.w0 + G::kBandWords == L.WW;
+  auto set_band = [&](int b) {
+    L.w0 = b * G::kBandWords;
+    const int wl = L.w0 + L.lane * NW;
+    L.pad = wl < 4 ? G::kPadR + wl * 4 : (wl >= L.WW - 4 ? G::kPadL + (wl - (L.WW - 4)) * 4 : -1);
+    L.padx = (L.w0 + G::kBandWords == L.WW ? 1 : 0) | (L.w0 == 0 ? 2 : 0) | (L.WW << 2);
+    L.pad_band = L.w0 == 0 || L.w0 + G::kBandWords == L.WW;
+  };
+  set_band(bA);
   const uint32_t stage = sbase + RG::kStageOff + warp * G::kStageAll;
   Ctx<NW, FORCE> cx;
   cx.kc = kc_base;
@@ -795,48 +836,65 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   unsigned swaps = 0;
   const uint32_t lane_off = 16u + lane * NW * 4u;
   const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
-  for (int r = R0 + warp; r < R1; r += RG::kCons) {
-    const uint32_t i = static_cast<uint32_t>(r - R0);  // ring index of source row r - 1
-    constexpr uint32_t kG = RG::kGroups, B = RG::kBox;
-    uint32_t sl[3];
+  // Destination rows [Rb, Re) of the current band, warp-interleaved; source
+  // row r - 1 sits at ring index ibase + r - Rb. Inlined once per part (one
+  // copy inside a loop over the parts measured 8% slower: spills).
+  auto rows = [&](const int Rb, const int Re, const uint32_t ibase) {
+    for (int r = Rb + warp; r < Re; r += RG::kCons) {
+      const uint32_t i = ibase + static_cast<uint32_t>(r - Rb);  // ring index of source row r - 1
+      const bool first_row = r == Rb, last_row = r == Re - 1;
+      constexpr uint32_t kG = RG::kGroups;
+      uint32_t sl[3];
 #pragma unroll
-    for (uint32_t d = 0; d < 3; ++d) {
-      const uint32_t P = (i + d) / B;
-      if (d == 0 || ((i + d) % B) == 0) {  // a new group
-        const uint32_t kp = P % kG;
-        for (;;) {
-          uint32_t tag;
-          asm volatile("ld.relaxed.cta.shared.u32 %0, [%1];" : "=r"(tag) : "r"(tags + kp * 4) : "memory");
-          if (tag == P) break;
-          __nanosleep(FHPG_TAG_SLEEP);
+      for (uint32_t d = 0; d < 3; ++d) {
+        const uint32_t P = (i + d) / B;
+        if (d == 0 || ((i + d) % B) == 0) {  // a new group
+          const uint32_t kp = P % kG;
+          for (;;) {
+            uint32_t tag;
+            asm volatile("ld.relaxed.cta.shared.u32 %0, [%1];"
+                         : "=r"(tag) : "r"(tags + kp * 4) : "memory");
+            if (tag == P) break;
+            __nanosleep(FHPG_TAG_SLEEP);
+          }
+          mbar_wait(full + kp * 8, (P / kG) & 1u);
         }
-        mbar_wait(full + kp * 8, (P / kG) & 1u);
+        sl[d] = ring + ((i + d) % RG::kRing) * G::kSlot + lane_off;
       }
-      sl[d] = ring + ((i + d) % RG::kRing) * G::kSlot + lane_off;
-    }
-    // Release the three source rows as soon as they are in registers (3
-    // consumers per row; segment edges make up for the destination rows
-    // outside [R0, R1)); one arrive per group the rows fall in.
-    auto release = [&] {
-      __syncwarp();
-      if (lane == 0) {
-        const uint32_t first = r == R0 ? 1u : 0u, lastr = r == R1 - 1 ? 1u : 0u;
-        const uint32_t c0 = 1 + 2 * first, c1 = 1 + first + lastr, c2 = 1 + 2 * lastr;
-        const uint32_t g0 = i / B, g1 = (i + 1) / B, g2 = (i + 2) / B;
-        if (g0 == g2) {
-          mbar_arrive(empty + (g0 % kG) * 8, c0 + c1 + c2);
-        } else {
-          mbar_arrive(empty + (g0 % kG) * 8, c0 + (g1 == g0 ? c1 : 0u));
-          mbar_arrive(empty + (g2 % kG) * 8, c2 + (g1 == g2 ? c1 : 0u));
+      // Release the three source rows as soon as they are in registers (3
+      // consumers per row; segment edges make up for the destination rows
+      // outside [Rb, Re)); one arrive per group the rows fall in.
+      auto release = [&] {
+        __syncwarp();
+        if (lane == 0) {
+          const uint32_t first = first_row ? 1u : 0u, lastr = last_row ? 1u : 0u;
+          const uint32_t c0 = 1 + 2 * first, c1 = 1 + first + lastr, c2 = 1 + 2 * lastr;
+          const uint32_t g0 = i / B, g1 = (i + 1) / B, g2 = (i + 2) / B;
+          if (g0 == g2) {
+            mbar_arrive(empty + (g0 % kG) * 8, c0 + c1 + c2);
+          } else {
+            mbar_arrive(empty + (g0 % kG) * 8, c0 + (g1 == g0 ? c1 : 0u));
+            mbar_arrive(empty + (g2 % kG) * 8, c2 + (g1 == g2 ? c1 : 0u));
+          }
         }
+      };
+      if ((a.row0 + r) & 1)
+        dest_row<NW, FORCE, 1>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
+                               L.pad, L.padx, L.pad_band, swaps, release);
+      else
+        dest_row<NW, FORCE, 0>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
+                               L.pad, L.padx, L.pad_band, swaps, release);
       }
-    };
-    if ((a.row0 + r) & 1)
-      dest_row<NW, FORCE, 1>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
-                             L.pad, L.padx, L.pad_band, swaps, release);
-    else
-      dest_row<NW, FORCE, 0>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
-                             L.pad, L.padx, L.pad_band, swaps, release);
+  };
+  rows(RA0, RA0 + nA, 0u);
+  if (nB > 0) {
+    // Extra CTA: on to band bA + 1 once every consumer is done with band bA
+    // (the key table is rewritten); the producer streams on meanwhile.
+    asm volatile("bar.sync 1, %0;" ::"r"(RG::kCons * 32) : "memory");
+    make_keys(bA + 1, threadIdx.x, RG::kCons * 32);
+    asm volatile("bar.sync 1, %0;" ::"r"(RG::kCons * 32) : "memory");
+    set_band(bA + 1);
+    rows(row_lo, row_lo + nB, offB);
   }
   if (lane == 0) bulk_wait_all();  // the stores have landed before the kernel ends
   if (FORCE) {
@@ -861,7 +919,26 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
   seg_groups = (rows + seg - 1) / seg;
   a.segs1 = seg_groups;
   const int rows2 = a.row_hi2 > a.row_lo2 ? a.row_hi2 - a.row_lo2 : 0;
-  const int grid = a.nbands * (seg_groups + (rows2 + seg - 1) / seg);
+  a.segs2 = (rows2 + seg - 1) / seg;
+  a.extra_rows = 0;
+  int grid = a.nbands * (seg_groups + a.segs2);
+  // SMs left over by nbands x segment groups (148 - 8 x 18 = 4 at W = 16384)
+  // take the last rows of two bands each, so that every SM has the same work:
+  // x rows per band go to them, x(2S + 1) = rows - S b with b rows of
+  // equivalent cost for their mid-kernel band switch.
+  const int spare = num_sms - a.nbands * (num_sms / a.nbands);
+  if (FHPG_EXTRA_CTAS && rows2 == 0 && a.nbands % 2 == 0 && 2 * spare >= a.nbands &&
+      num_sms / a.nbands >= 2) {
+    const int S = num_sms / a.nbands;
+    const int x = (rows - FHPG_EXTRA_BUBBLE_ROWS * S) / (2 * S + 1);
+    if (x >= 16) {
+      a.extra_rows = x;
+      a.seg_rows = (rows - x + S - 1) / S;
+      a.segs1 = (rows - x + a.seg_rows - 1) / a.seg_rows;
+      a.segs2 = 0;
+      grid = a.nbands * a.segs1 + a.nbands / 2;
+    }
+  }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(step_ring_kernel<NW, FORCE>, cudaFuncAttributeMaxDynamicSharedMemorySize,

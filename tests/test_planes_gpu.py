@@ -251,3 +251,20 @@ def test_ring_carry_columns(port, tables):
         out = e.download()
         assert (out == ref).all(), (st, [f for f in found if f[0] == st], np.argwhere(out != ref)[:5])
 
+
+
+@pytest.mark.parametrize("W,H,fp", [(16384, 1100, 0.0), (16384, 1100, 0.3), (12288, 1500, 0.05),
+                                    (16384, 2000, 1.0)])
+def test_ring_extra_ctas(W, H, fp, port, tables):
+    """Widths whose band count leaves SMs over (8 bands x 18 segments = 144
+    of 148 SMs at W = 16384; 6 x 24 at 12288): the spare CTAs take the last
+    rows of two bands each, switching bands mid-kernel (key table rebuilt
+    behind a consumer barrier, ring continuing across the switch)."""
+    s, m = port.scramble(W, H, W + H)
+    e = engine(W, H, tables["fhp3"], m, s)
+    assert e.path == "planes"
+    sw = e.advance(11, fp, 77, 3)
+    ref, rsw = port.advance(s, tables["fhp3"], 11, port.threshold(fp), 77, 3, mask=m)
+    out = e.download()
+    assert (out == ref).all(), np.argwhere(out != ref)[:5]
+    assert sw == rsw
