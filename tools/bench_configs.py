@@ -69,6 +69,7 @@ if __name__ == "__main__":
            timed(4096, 2048, "fhp3", 0.01, 1000, 2, 0.2),
            timed(8192, 4096, "fhp3", 0.01, 500, 3, 0.2, mask=cylinder_mask(8192, 4096)),
            timed(16384, 16384, "fhp3", 0.0, 200, 4, 0.2),
+           timed(16384, 16384, "fhp3", 0.01, 100, 4, 0.2),
            timed(16384, 16384, "default", 0.0, 200, 4, 0.2)]
     for o in out:
         print(json.dumps(o))
