@@ -25,6 +25,7 @@ struct fhpg_engine {
   // step, an unpacked copy afterwards).
   bool planes = false;
   bool table_planes = false;
+  int planes_rule = 2;                   // circuit of the table: 2 = FHP-III, 0 = DEFAULT
   int path_pref = 0;                     // 0 auto, 1 byte fast path, 2 generic
   uint8_t* scratch = nullptr;            // nrows * pitch
   alignas(64) unsigned char tmap[2][4][128];  // TMA descriptors of buf[0], buf[1] (planes)
@@ -264,6 +265,7 @@ void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64
     a.kf_cur = step_key(seed, kForcing, s);
     a.thr = thr;
     a.swaps = e->swaps;
+    a.rule = e->planes_rule;
     if (i + 1 < count) {
       a.zc_next = e->keys((s + 1) & 1, 0);
       a.zf_next = force ? e->keys((s + 1) & 1, 1) : nullptr;
@@ -316,6 +318,7 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
   a.kf_cur = step_key(seed, kForcing, s);
   a.thr = thr;
   a.swaps = e->swaps;
+  a.rule = e->planes_rule;
   const bool interior = e->nrows >= 3;
   auto run = [&](int lo, int hi, bool with_next_keys) {
     StepArgs b = a;
@@ -411,10 +414,13 @@ int fhpg_set_table(fhpg_engine* e, const uint8_t* t) {
     ck(cudaMemcpyAsync(e->table, t, 512, cudaMemcpyHostToDevice, e->stream), "table upload");
     ck(cudaStreamSynchronize(e->stream), "table upload sync");
     e->table_set = true;
-    // The bit-plane kernel evaluates FHP-III as a circuit (fhpg_planes_rules.cuh).
-    uint8_t fhp3[512];
+    // The bit-plane kernels evaluate FHP-III and the reference's DEFAULT rule
+    // as circuits (fhpg_planes_rules.cuh); any other table runs the byte LUT path.
+    uint8_t fhp3[512], def[512];
     fhpg_build_table(FHPG_RULES_FHP_III, fhp3);
-    e->table_planes = std::memcmp(t, fhp3, 512) == 0;
+    fhpg_build_table(FHPG_RULES_DEFAULT, def);
+    e->table_planes = std::memcmp(t, fhp3, 512) == 0 || std::memcmp(t, def, 512) == 0;
+    e->planes_rule = std::memcmp(t, fhp3, 512) == 0 ? 2 : 0;
     sync_layout(e);
   });
 }

@@ -43,6 +43,7 @@ struct StepArgs {
   int segs1 = 0;             // row segments of the first range (bit-plane ring kernel)
   int segs2 = 0;             //   ... of the second range
   int extra_rows = 0;        // ring kernel: last rows of every band done by the extra CTAs
+  int rule = 2;              // bit-plane kernels: collision circuit, 2 = FHP-III, 0 = DEFAULT
 };
 
 // Fast path launcher (fhpg_step_fast.cu).
@@ -62,7 +63,7 @@ size_t planes_row_bytes(int W);
 // loads (band + edge words, 8 planes), 1 = band stores (7 planes), 2 = pad
 // stores (4 words, 7 planes), 3 = two-row loads.
 bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows, int kind);
-// One time step with the FHP-III circuit over rows [row_lo, row_hi): loads
+// One time step with a collision circuit (a.rule) over rows [row_lo, row_hi): loads
 // through the source buffer's kind-0 map, stores through the destination
 // buffer's kind-1 / kind-2 maps.
 int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap_dst_store,

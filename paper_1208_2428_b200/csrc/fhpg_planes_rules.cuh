@@ -153,4 +153,63 @@ FHPG_HD void fhp3_apply(const Fhp3Class& k, uint32_t c, uint32_t r, const uint32
   o_r = lop3<FHPG_LUT(kLA ^ (kLB | kLC))>(r, U, k.AY);
 }
 
+// The reference's own rule (RuleVariant::Default, collision.cpp:22-72) as a
+// circuit, ~63 LOP3 per 32 sites. Fluid classes by axis signals O_k = a_k ^
+// a_{k+3} (odd axis) and P_k = a_k & a_{k+3} (pair):
+//   HO head-on pair, no rest (no odd axis, exactly one pair): rotate by 1
+//      (chirality 1) or 2 (chirality 0)                      collision.cpp:29-31
+//   TB symmetric triple, no rest (three odd axes, a0 == a2 == a4): complement
+//                                                            collision.cpp:33-35
+//   RA one mover + rest (one odd axis, no pair): {i}+R -> {i-1, i+1}  :37-41
+//   RC two movers 120 deg apart, no rest (two odd axes, no pair, an even
+//      number of them on odd directions): {i, i+2} -> {i+1}+R        :43-51
+//   obstacles bounce back, rest kept                                   :59-63
+// Only HO depends on the chirality.
+struct DefClass {
+  uint32_t HO, TB, RA, RC, KEEP;
+  uint32_t dep;
+};
+
+FHPG_HD DefClass def_classify(const uint32_t a[6], uint32_t r, uint32_t s) {
+  DefClass k;
+  const uint32_t O0 = a[0] ^ a[3], O1 = a[1] ^ a[4], O2 = a[2] ^ a[5];
+  const uint32_t P0 = a[0] & a[3], P1 = a[1] & a[4], P2 = a[2] & a[5];
+  const uint32_t rs = r | s;
+  constexpr uint32_t kOne = FHPG_LUT((kLA ^ kLB ^ kLC) & ~(kLA & kLB & kLC));
+  constexpr uint32_t kTwo = FHPG_LUT(((kLA & kLB) | (kLA & kLC) | (kLB & kLC)) & ~(kLA & kLB & kLC));
+  const uint32_t noO = lop3<kNor3>(O0, O1, O2);
+  const uint32_t oneP = lop3<kOne>(P0, P1, P2);
+  const uint32_t anyP = lop3<kOr3>(P0, P1, P2);
+  const uint32_t ex1 = lop3<kOne>(O0, O1, O2);
+  const uint32_t ex2 = lop3<kTwo>(O0, O1, O2);
+  const uint32_t O3 = lop3<FHPG_LUT(kLA & kLB & kLC)>(O0, O1, O2);
+  const uint32_t eqv = lop3<FHPG_LUT((kLA & kLB & kLC) | (~kLA & ~kLB & ~kLC))>(a[0], a[2], a[4]);
+  const uint32_t pi = lop3<kXor3>(a[1], a[3], a[5]);
+  constexpr uint32_t kAnB_nC = FHPG_LUT(kLA & kLB & ~kLC);
+  k.HO = lop3<kAnB_nC>(noO, oneP, rs);
+  k.TB = lop3<kAnB_nC>(O3, eqv, rs);
+  k.RA = lop3<FHPG_LUT(kLA & ~kLB & kLC)>(ex1, anyP, r) & ~s;
+  k.RC = lop3<FHPG_LUT(kLA & ~kLB & ~kLC)>(ex2, anyP, rs) & ~pi;
+  const uint32_t u = lop3<kOr3>(k.HO, k.TB, k.RA);
+  k.KEEP = lop3<kNor3>(u, k.RC, s);
+  k.dep = k.HO;
+  return k;
+}
+
+FHPG_HD void def_apply(const DefClass& k, uint32_t c, uint32_t r, const uint32_t a[6],
+                       uint32_t o[6], uint32_t& o_r, uint32_t s) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const uint32_t am1 = a[(i + 5) % 6], ap1 = a[(i + 1) % 6];
+    const uint32_t rot = lop3<kMux>(c, am1, a[(i + 4) % 6]);   // c ? a_{i-1} : a_{i-2}
+    const uint32_t t = lop3<FHPG_LUT((kLA & ~kLC) | (kLB & kLC))>(k.TB, k.KEEP, a[i]);
+    const uint32_t acc = lop3<kAndOr>(k.HO, rot, t);
+    const uint32_t ua = lop3<FHPG_LUT((kLA | kLB) & kLC)>(am1, ap1, k.RA);
+    const uint32_t vc = lop3<FHPG_LUT(kLA & kLB & kLC)>(am1, ap1, k.RC);
+    const uint32_t acc2 = lop3<kOr3>(acc, ua, vc);
+    o[i] = lop3<kAndOr>(s, a[(i + 3) % 6], acc2);
+  }
+  o_r = lop3<FHPG_LUT((kLA & ~kLB) | kLC)>(r, k.RA, k.RC);
+}
+
 }  // namespace fhpg

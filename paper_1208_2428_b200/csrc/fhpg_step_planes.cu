@@ -54,6 +54,35 @@ namespace fhpg {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// Collision circuits the bit-plane kernels evaluate (fhpg_planes_rules.cuh):
+// RULE 2 = FHP-III, RULE 0 = the reference's DEFAULT rule.
+template <int RULE>
+struct PlaneRule;
+template <>
+struct PlaneRule<2> {
+  using Class = Fhp3Class;
+  static __device__ __forceinline__ Class classify(const uint32_t a[6], uint32_t r, uint32_t s) {
+    return fhp3_classify(a, r, s);
+  }
+  static __device__ __forceinline__ void apply(const Class& k, uint32_t c, uint32_t r,
+                                               const uint32_t a[6], uint32_t o[6], uint32_t& o_r,
+                                               uint32_t) {
+    fhp3_apply(k, c, r, a, o, o_r);
+  }
+};
+template <>
+struct PlaneRule<0> {
+  using Class = DefClass;
+  static __device__ __forceinline__ Class classify(const uint32_t a[6], uint32_t r, uint32_t s) {
+    return def_classify(a, r, s);
+  }
+  static __device__ __forceinline__ void apply(const Class& k, uint32_t c, uint32_t r,
+                                               const uint32_t a[6], uint32_t o[6], uint32_t& o_r,
+                                               uint32_t s) {
+    def_apply(k, c, r, a, o, o_r, s);
+  }
+};
 // Warps per CTA (one CTA per SM): 16 with 2 words per lane, 8 with 4.
 #ifndef FHPG_STREAM_ONLY
 #define FHPG_STREAM_ONLY 0  // timing experiments (wrong results): 1 memory pipeline only,
@@ -372,7 +401,7 @@ struct Ctx {
 // of the slots of rows r-1, r, r+1; Q = global parity of r.
 // `released()` is called once the source rows have been read into
 // registers (the ring slots may be refilled from then on).
-template <int NW, bool FORCE, int Q, typename Rel>
+template <int NW, bool FORCE, int RULE, int Q, typename Rel>
 __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
                                          const Ctx<NW, FORCE>& cx, int lane, uint32_t y,
                                          const CUtensorMap* stmap, const CUtensorMap* padmap,
@@ -419,12 +448,12 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   (void)swaps; (void)y; (void)pad; (void)padx; (void)pad_band; (void)padmap;
   return;
 #endif
-  Fhp3Class K[NW];
+  typename PlaneRule<RULE>::Class K[NW];
   uint32_t dep[NW];
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
     const uint32_t a[6] = {a0[w], a1[w], a2[w], a3[w], a4[w], a5[w]};
-    K[w] = fhp3_classify(a, rr[w], so[w]);
+    K[w] = PlaneRule<RULE>::classify(a, rr[w], so[w]);
     dep[w] = K[w].dep;
   }
   // The previous row's TMA store must have read the staging area (which
@@ -443,7 +472,7 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
     const uint32_t c = T ? lds32(mine + w * 4) : 0u;
     uint32_t oo[6], orr;
     const uint32_t a[6] = {a0[w], a1[w], a2[w], a3[w], a4[w], a5[w]};
-    fhp3_apply(K[w], c, rr[w], a, oo, orr);
+    PlaneRule<RULE>::apply(K[w], c, rr[w], a, oo, orr, so[w]);
 #pragma unroll
     for (int p = 0; p < 6; ++p) o[w][p] = oo[p];
     o[w][6] = orr;
@@ -489,7 +518,7 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn,
   }
 }
 
-template <int NW, bool FORCE, int Q0>
+template <int NW, bool FORCE, int RULE, int Q0>
 __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap* map,
                                             const CUtensorMap* stmap, const CUtensorMap* padmap,
                                             const Lanes& L, uint32_t ring, uint32_t bars,
@@ -526,7 +555,7 @@ __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap
   auto one = [&](int r, auto qc) {
     constexpr int Q = decltype(qc)::value;
     wait(sn);
-    dest_row<NW, FORCE, Q>(ring + sm * G::kSlot + lane_off, ring + sc * G::kSlot + lane_off,
+    dest_row<NW, FORCE, RULE, Q>(ring + sm * G::kSlot + lane_off, ring + sc * G::kSlot + lane_off,
                            ring + sn * G::kSlot + lane_off, cx, L.lane, y0 + r, stmap, padmap,
                            L.w0, r + 1, L.pad, L.padx, L.pad_band, swaps, [] {});
     // The slot of row r-1 is free once every lane has read it.
@@ -548,7 +577,7 @@ __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap
   if (L.lane == 0) bulk_wait_all();  // the stores have landed before the kernel ends
 }
 
-template <int NW, bool FORCE>
+template <int NW, bool FORCE, int RULE>
 __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
     step_planes_kernel(StepArgs a, const __grid_constant__ CUtensorMap map,
                        const __grid_constant__ CUtensorMap stmap,
@@ -618,9 +647,9 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
   cx.four = a.k4;
   unsigned swaps = 0;
   if ((a.row0 + r_begin) & 1)
-    run_segment<NW, FORCE, 1>(a, &map, &stmap, &padmap, L, ring, bars, cx, r_begin, r_end, swaps);
+    run_segment<NW, FORCE, RULE, 1>(a, &map, &stmap, &padmap, L, ring, bars, cx, r_begin, r_end, swaps);
   else
-    run_segment<NW, FORCE, 0>(a, &map, &stmap, &padmap, L, ring, bars, cx, r_begin, r_end, swaps);
+    run_segment<NW, FORCE, RULE, 0>(a, &map, &stmap, &padmap, L, ring, bars, cx, r_begin, r_end, swaps);
   if (FORCE) {
     unsigned long long s = swaps;
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
@@ -692,7 +721,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 
-template <int NW, bool FORCE>
+template <int NW, bool FORCE, int RULE>
 __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
     step_ring_kernel(StepArgs a, const __grid_constant__ CUtensorMap map,
                      const __grid_constant__ CUtensorMap stmap,
@@ -882,10 +911,10 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
         }
       };
       if ((a.row0 + r) & 1)
-        dest_row<NW, FORCE, 1>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
+        dest_row<NW, FORCE, RULE, 1>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
                                L.pad, L.padx, L.pad_band, swaps, release);
       else
-        dest_row<NW, FORCE, 0>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
+        dest_row<NW, FORCE, RULE, 0>(sl[0], sl[1], sl[2], cx, lane, y0 + r, &stmap, &padmap, L.w0, r + 1,
                                L.pad, L.padx, L.pad_band, swaps, release);
       }
   };
@@ -907,7 +936,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   }
 }
 
-template <int NW, bool FORCE>
+template <int NW, bool FORCE, int RULE>
 void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st) {
   using G = Geo<NW, FORCE>;
   using RG = RingGeo<NW, FORCE>;
@@ -944,7 +973,7 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(step_ring_kernel<NW, FORCE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(step_ring_kernel<NW, FORCE, RULE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          RG::kSmem);
     attr = true;
   }
@@ -962,9 +991,9 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, step_ring_kernel<NW, FORCE>, a, maps[0], maps[1], maps[2], maps[3]);
+  cudaLaunchKernelEx(&cfg, step_ring_kernel<NW, FORCE, RULE>, a, maps[0], maps[1], maps[2], maps[3]);
 #else
-  step_ring_kernel<NW, FORCE><<<grid, RG::kThreads, RG::kSmem, st>>>(a, maps[0], maps[1], maps[2],
+  step_ring_kernel<NW, FORCE, RULE><<<grid, RG::kThreads, RG::kSmem, st>>>(a, maps[0], maps[1], maps[2],
                                                                      maps[3]);
 #endif
 }
@@ -975,7 +1004,7 @@ int smem_bytes(int bpc) {
   return (FORCE ? 2 : 1) * bpc * G::kBandCols * 8 + kPWarps<NW> * G::kWarp;
 }
 
-template <int NW, bool FORCE>
+template <int NW, bool FORCE, int RULE>
 void launch_nw(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st) {
   using G = Geo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
@@ -1003,11 +1032,11 @@ void launch_nw(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st
   // machinery, so the dynamic opt-in is set to exactly what is used.)
   static int attr = -1;
   if (attr != smem) {
-    cudaFuncSetAttribute(step_planes_kernel<NW, FORCE>,
+    cudaFuncSetAttribute(step_planes_kernel<NW, FORCE, RULE>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = smem;
   }
-  step_planes_kernel<NW, FORCE><<<grid, kWarps * 32, smem, st>>>(a, maps[0], maps[1], maps[2]);
+  step_planes_kernel<NW, FORCE, RULE><<<grid, kWarps * 32, smem, st>>>(a, maps[0], maps[1], maps[2]);
 }
 
 // ---------------------------------------------------------------------------
@@ -1142,10 +1171,29 @@ int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap
                             *static_cast<const CUtensorMap*>(tmap_dst_store),
                             *static_cast<const CUtensorMap*>(tmap_dst_pad),
                             *static_cast<const CUtensorMap*>(tmap_src_pair)};
+  // a.rule: 2 = FHP-III, 0 = DEFAULT (the circuit the kernels instantiate)
+  auto ring = [&](auto rule) {
+    constexpr int R = decltype(rule)::value;
+    if (force) launch_ring<2, true, R>(a, m, num_sms, st);
+    else launch_ring<2, false, R>(a, m, num_sms, st);
+  };
+  auto nwk = [&](auto rule) {
+    constexpr int R = decltype(rule)::value;
+    if (nw == 4) {
+      if (force) launch_nw<4, true, R>(a, m, num_sms, st);
+      else launch_nw<4, false, R>(a, m, num_sms, st);
+    } else if (nw == 2) {
+      if (force) launch_nw<2, true, R>(a, m, num_sms, st);
+      else launch_nw<2, false, R>(a, m, num_sms, st);
+    } else {
+      if (force) launch_nw<1, true, R>(a, m, num_sms, st);
+      else launch_nw<1, false, R>(a, m, num_sms, st);
+    }
+  };
 #if FHPG_PLANES_RING
   if (nw == 2) {
-    if (force) launch_ring<2, true>(a, m, num_sms, st);
-    else launch_ring<2, false>(a, m, num_sms, st);
+    if (a.rule == 0) ring(std::integral_constant<int, 0>{});
+    else ring(std::integral_constant<int, 2>{});
     return 1;
   }
 #endif
@@ -1159,16 +1207,8 @@ int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap
            launch_step_planes(a2, tmap_src, tmap_dst_store, tmap_dst_pad, tmap_src_pair, num_sms,
                               st);
   }
-  if (nw == 4) {
-    if (force) launch_nw<4, true>(a, m, num_sms, st);
-    else launch_nw<4, false>(a, m, num_sms, st);
-  } else if (nw == 2) {
-    if (force) launch_nw<2, true>(a, m, num_sms, st);
-    else launch_nw<2, false>(a, m, num_sms, st);
-  } else {
-    if (force) launch_nw<1, true>(a, m, num_sms, st);
-    else launch_nw<1, false>(a, m, num_sms, st);
-  }
+  if (a.rule == 0) nwk(std::integral_constant<int, 0>{});
+  else nwk(std::integral_constant<int, 2>{});
   return 1;
 }
 

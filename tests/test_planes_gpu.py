@@ -30,7 +30,8 @@ def engine(W, H, table, mask=None, state=None, path="auto"):
 def test_path_selection(tables):
     assert engine(1024, 8, tables["fhp3"]).path == "planes"
     assert engine(16384, 8, tables["fhp3"]).path == "planes"
-    assert engine(1024, 8, tables["default"]).path == "bytes"
+    assert engine(1024, 8, tables["default"]).path == "planes"  # the reference's rule as a circuit
+    assert engine(1024, 8, tables["fhp1"]).path == "bytes"
     assert engine(1056, 8, tables["fhp3"]).path == "bytes"
     assert engine(1024, 8, tables["fhp3"], path="bytes").path == "bytes"
     assert engine(1024, 8, tables["fhp3"], path="generic").path == "generic"
@@ -100,7 +101,7 @@ def test_layout_switches_mid_run(port, tables):
     step = 100
     for name, n in plan:
         e.set_table(tables[name])
-        assert e.path == ("planes" if name == "fhp3" else "bytes")
+        assert e.path == ("planes" if name in ("fhp3", "default") else "bytes")
         sw = e.advance(3, 0.2, step, n)
         ref, rsw = port.advance(ref, tables[name], 3, port.threshold(0.2), step, n, mask=m)
         assert (e.download() == ref).all(), name
@@ -267,4 +268,30 @@ def test_ring_extra_ctas(W, H, fp, port, tables):
     ref, rsw = port.advance(s, tables["fhp3"], 11, port.threshold(fp), 77, 3, mask=m)
     out = e.download()
     assert (out == ref).all(), np.argwhere(out != ref)[:5]
+    assert sw == rsw
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_default_rule_planes_against_oracle(case, port, tables):
+    """The reference's own DEFAULT rule on the bit-plane path (its circuit,
+    def_classify / def_apply): adversarial states, obstacles, forcing up to
+    p = 1, nonzero first_step, every kernel (W = 1024 per-warp, >= 4096
+    ring, 16384 x 1100 ring with the extra-CTA split)."""
+    rng = np.random.default_rng(9100 + case)
+    if case == 15:
+        W, H = 16384, 1100
+    else:
+        W = int(rng.choice([1024, 2048, 4096, 6144]))
+        H = int(rng.choice([3, 5, 37, 64, 131]))
+    fp = float(rng.choice([0.0, 0.0, 0.01, 0.3, 1.0]))
+    seed = int(rng.integers(0, 2**63))
+    steps = int(rng.integers(1, 9))
+    first = int(rng.integers(0, 10**6))
+    s, m = port.scramble(W, H, seed)
+    ref, rsw = port.advance(s, tables["default"], seed, port.threshold(fp), first, steps, mask=m)
+    e = engine(W, H, tables["default"], m, s)
+    assert e.path == "planes"
+    sw = e.advance(seed, fp, first, steps)
+    out = e.download()
+    assert (out == ref).all(), (W, H, fp, steps, np.argwhere(out != ref)[:5])
     assert sw == rsw

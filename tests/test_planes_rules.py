@@ -19,4 +19,5 @@ def test_planes_circuits_match_tables(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "fhp3: ok (48 dep states)" in out.stdout
+    assert "default: ok (3 dep states)" in out.stdout
     assert "chir_bit: ok" in out.stdout
