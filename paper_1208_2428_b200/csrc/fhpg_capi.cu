@@ -25,7 +25,7 @@ struct fhpg_engine {
   // step, an unpacked copy afterwards).
   bool planes = false;
   bool table_planes = false;
-  int planes_rule = 2;                   // circuit of the table: 2 = FHP-III, 0 = DEFAULT
+  int planes_rule = 2;                   // circuit of the table: FHPG_RULES_* (fhpg_tables.h)
   int path_pref = 0;                     // 0 auto, 1 byte fast path, 2 generic
   uint8_t* scratch = nullptr;            // nrows * pitch
   alignas(64) unsigned char tmap[2][4][128];  // TMA descriptors of buf[0], buf[1] (planes)
@@ -414,13 +414,19 @@ int fhpg_set_table(fhpg_engine* e, const uint8_t* t) {
     ck(cudaMemcpyAsync(e->table, t, 512, cudaMemcpyHostToDevice, e->stream), "table upload");
     ck(cudaStreamSynchronize(e->stream), "table upload sync");
     e->table_set = true;
-    // The bit-plane kernels evaluate FHP-III and the reference's DEFAULT rule
-    // as circuits (fhpg_planes_rules.cuh); any other table runs the byte LUT path.
-    uint8_t fhp3[512], def[512];
-    fhpg_build_table(FHPG_RULES_FHP_III, fhp3);
-    fhpg_build_table(FHPG_RULES_DEFAULT, def);
-    e->table_planes = std::memcmp(t, fhp3, 512) == 0 || std::memcmp(t, def, 512) == 0;
-    e->planes_rule = std::memcmp(t, fhp3, 512) == 0 ? 2 : 0;
+    // The bit-plane kernels evaluate FHP-III, FHP-I and the reference's
+    // DEFAULT rule as circuits (fhpg_planes_rules.cuh); any other table runs
+    // the byte LUT path.
+    e->table_planes = false;
+    for (const int v : {FHPG_RULES_FHP_III, FHPG_RULES_FHP_I, FHPG_RULES_DEFAULT}) {
+      uint8_t ref[512];
+      fhpg_build_table(v, ref);
+      if (std::memcmp(t, ref, 512) == 0) {
+        e->table_planes = true;
+        e->planes_rule = v;
+        break;
+      }
+    }
     sync_layout(e);
   });
 }

@@ -43,7 +43,8 @@ struct StepArgs {
   int segs1 = 0;             // row segments of the first range (bit-plane ring kernel)
   int segs2 = 0;             //   ... of the second range
   int extra_rows = 0;        // ring kernel: last rows of every band done by the extra CTAs
-  int rule = 2;              // bit-plane kernels: collision circuit, 2 = FHP-III, 0 = DEFAULT
+  int rule = 2;              // bit-plane kernels: collision circuit, 2 = FHP-III, 1 = FHP-I,
+                             // 0 = DEFAULT (FHPG_RULES_*)
 };
 
 // Fast path launcher (fhpg_step_fast.cu).

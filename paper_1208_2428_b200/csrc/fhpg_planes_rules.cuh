@@ -212,4 +212,42 @@ FHPG_HD void def_apply(const DefClass& k, uint32_t c, uint32_t r, const uint32_t
   o_r = lop3<FHPG_LUT((kLA & ~kLB) | kLC)>(r, k.RA, k.RC);
 }
 
+// FHP-I (fhpg_tables.cpp build_fhp1): head-on pairs without rest rotate by
+// +60 (chirality 1) or -60 degrees (chirality 0), symmetric triples without
+// rest complement, obstacles bounce back; ~30 LOP3 per 32 sites.
+struct Fhp1Class {
+  uint32_t HO, TB, KEEP;
+  uint32_t dep;
+};
+
+FHPG_HD Fhp1Class fhp1_classify(const uint32_t a[6], uint32_t r, uint32_t s) {
+  Fhp1Class k;
+  const uint32_t O0 = a[0] ^ a[3], O1 = a[1] ^ a[4], O2 = a[2] ^ a[5];
+  const uint32_t P0 = a[0] & a[3], P1 = a[1] & a[4], P2 = a[2] & a[5];
+  const uint32_t rs = r | s;
+  constexpr uint32_t kOne = FHPG_LUT((kLA ^ kLB ^ kLC) & ~(kLA & kLB & kLC));
+  const uint32_t noO = lop3<kNor3>(O0, O1, O2);
+  const uint32_t oneP = lop3<kOne>(P0, P1, P2);
+  const uint32_t O3 = lop3<FHPG_LUT(kLA & kLB & kLC)>(O0, O1, O2);
+  const uint32_t eqv = lop3<FHPG_LUT((kLA & kLB & kLC) | (~kLA & ~kLB & ~kLC))>(a[0], a[2], a[4]);
+  constexpr uint32_t kAnB_nC = FHPG_LUT(kLA & kLB & ~kLC);
+  k.HO = lop3<kAnB_nC>(noO, oneP, rs);
+  k.TB = lop3<kAnB_nC>(O3, eqv, rs);
+  k.KEEP = lop3<kNor3>(k.HO, k.TB, s);
+  k.dep = k.HO;
+  return k;
+}
+
+FHPG_HD void fhp1_apply(const Fhp1Class& k, uint32_t c, uint32_t r, const uint32_t a[6],
+                        uint32_t o[6], uint32_t& o_r, uint32_t s) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    const uint32_t rot = lop3<kMux>(c, a[(i + 5) % 6], a[(i + 1) % 6]);  // c ? a_{i-1} : a_{i+1}
+    const uint32_t t = lop3<FHPG_LUT((kLA & ~kLC) | (kLB & kLC))>(k.TB, k.KEEP, a[i]);
+    const uint32_t acc = lop3<kAndOr>(k.HO, rot, t);
+    o[i] = lop3<kAndOr>(s, a[(i + 3) % 6], acc);
+  }
+  o_r = r;
+}
+
 }  // namespace fhpg

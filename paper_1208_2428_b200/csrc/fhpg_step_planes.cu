@@ -56,7 +56,7 @@ namespace {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 // Collision circuits the bit-plane kernels evaluate (fhpg_planes_rules.cuh):
-// RULE 2 = FHP-III, RULE 0 = the reference's DEFAULT rule.
+// RULE 2 = FHP-III, 1 = FHP-I, 0 = the reference's DEFAULT rule.
 template <int RULE>
 struct PlaneRule;
 template <>
@@ -69,6 +69,18 @@ struct PlaneRule<2> {
                                                const uint32_t a[6], uint32_t o[6], uint32_t& o_r,
                                                uint32_t) {
     fhp3_apply(k, c, r, a, o, o_r);
+  }
+};
+template <>
+struct PlaneRule<1> {
+  using Class = Fhp1Class;
+  static __device__ __forceinline__ Class classify(const uint32_t a[6], uint32_t r, uint32_t s) {
+    return fhp1_classify(a, r, s);
+  }
+  static __device__ __forceinline__ void apply(const Class& k, uint32_t c, uint32_t r,
+                                               const uint32_t a[6], uint32_t o[6], uint32_t& o_r,
+                                               uint32_t s) {
+    fhp1_apply(k, c, r, a, o, o_r, s);
   }
 };
 template <>
@@ -1171,7 +1183,7 @@ int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap
                             *static_cast<const CUtensorMap*>(tmap_dst_store),
                             *static_cast<const CUtensorMap*>(tmap_dst_pad),
                             *static_cast<const CUtensorMap*>(tmap_src_pair)};
-  // a.rule: 2 = FHP-III, 0 = DEFAULT (the circuit the kernels instantiate)
+  // a.rule: 2 = FHP-III, 1 = FHP-I, 0 = DEFAULT (the circuit the kernels instantiate)
   auto ring = [&](auto rule) {
     constexpr int R = decltype(rule)::value;
     if (force) launch_ring<2, true, R>(a, m, num_sms, st);
@@ -1193,6 +1205,7 @@ int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap
 #if FHPG_PLANES_RING
   if (nw == 2) {
     if (a.rule == 0) ring(std::integral_constant<int, 0>{});
+    else if (a.rule == 1) ring(std::integral_constant<int, 1>{});
     else ring(std::integral_constant<int, 2>{});
     return 1;
   }
@@ -1208,6 +1221,7 @@ int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap
                               st);
   }
   if (a.rule == 0) nwk(std::integral_constant<int, 0>{});
+  else if (a.rule == 1) nwk(std::integral_constant<int, 1>{});
   else nwk(std::integral_constant<int, 2>{});
   return 1;
 }

@@ -31,7 +31,10 @@ def test_path_selection(tables):
     assert engine(1024, 8, tables["fhp3"]).path == "planes"
     assert engine(16384, 8, tables["fhp3"]).path == "planes"
     assert engine(1024, 8, tables["default"]).path == "planes"  # the reference's rule as a circuit
-    assert engine(1024, 8, tables["fhp1"]).path == "bytes"
+    assert engine(1024, 8, tables["fhp1"]).path == "planes"
+    t = tables["fhp3"].copy()
+    t[3], t[5] = t[5], t[3]  # any other table: byte LUT path
+    assert engine(1024, 8, t).path == "bytes"
     assert engine(1056, 8, tables["fhp3"]).path == "bytes"
     assert engine(1024, 8, tables["fhp3"], path="bytes").path == "bytes"
     assert engine(1024, 8, tables["fhp3"], path="generic").path == "generic"
@@ -97,13 +100,17 @@ def test_layout_switches_mid_run(port, tables):
     s, m = port.scramble(W, H, 8)
     e = engine(W, H, tables["fhp3"], m, s)
     ref = s
-    plan = [("fhp3", 4), ("default", 3), ("fhp3", 5), ("fhp1", 2), ("fhp3", 6)]
+    custom = tables["fhp3"].copy()
+    custom[3], custom[5] = custom[5], custom[3]  # no circuit: byte LUT path
+    tabs = dict(tables, custom=custom)
+    plan = [("fhp3", 4), ("default", 3), ("custom", 3), ("fhp3", 5), ("fhp1", 2), ("custom", 2),
+            ("fhp3", 6)]
     step = 100
     for name, n in plan:
-        e.set_table(tables[name])
-        assert e.path == ("planes" if name in ("fhp3", "default") else "bytes")
+        e.set_table(tabs[name])
+        assert e.path == ("bytes" if name == "custom" else "planes")
         sw = e.advance(3, 0.2, step, n)
-        ref, rsw = port.advance(ref, tables[name], 3, port.threshold(0.2), step, n, mask=m)
+        ref, rsw = port.advance(ref, tabs[name], 3, port.threshold(0.2), step, n, mask=m)
         assert (e.download() == ref).all(), name
         assert sw == rsw
         step += n
@@ -272,9 +279,10 @@ def test_ring_extra_ctas(W, H, fp, port, tables):
 
 
 @pytest.mark.parametrize("case", range(16))
-def test_default_rule_planes_against_oracle(case, port, tables):
-    """The reference's own DEFAULT rule on the bit-plane path (its circuit,
-    def_classify / def_apply): adversarial states, obstacles, forcing up to
+@pytest.mark.parametrize("rule", ["default", "fhp1"])
+def test_other_rules_planes_against_oracle(rule, case, port, tables):
+    """The reference's own DEFAULT rule and FHP-I on the bit-plane path (their
+    circuits, def_* / fhp1_*): adversarial states, obstacles, forcing up to
     p = 1, nonzero first_step, every kernel (W = 1024 per-warp, >= 4096
     ring, 16384 x 1100 ring with the extra-CTA split)."""
     rng = np.random.default_rng(9100 + case)
@@ -288,8 +296,8 @@ def test_default_rule_planes_against_oracle(case, port, tables):
     steps = int(rng.integers(1, 9))
     first = int(rng.integers(0, 10**6))
     s, m = port.scramble(W, H, seed)
-    ref, rsw = port.advance(s, tables["default"], seed, port.threshold(fp), first, steps, mask=m)
-    e = engine(W, H, tables["default"], m, s)
+    ref, rsw = port.advance(s, tables[rule], seed, port.threshold(fp), first, steps, mask=m)
+    e = engine(W, H, tables[rule], m, s)
     assert e.path == "planes"
     sw = e.advance(seed, fp, first, steps)
     out = e.download()

@@ -20,4 +20,5 @@ def test_planes_circuits_match_tables(tmp_path):
     assert out.returncode == 0, out.stdout + out.stderr
     assert "fhp3: ok (48 dep states)" in out.stdout
     assert "default: ok (3 dep states)" in out.stdout
+    assert "fhp1: ok (3 dep states)" in out.stdout
     assert "chir_bit: ok" in out.stdout

@@ -84,6 +84,17 @@ int main() {
                [](const auto& k, uint32_t c, uint32_t r, const uint32_t* x_a, uint32_t* o, uint32_t& orr) {
                  def_apply(k, c, r, x_a, o, orr, k.solid);
                });
+  bad += check("fhp1", FHPG_RULES_FHP_I,
+               [](const uint32_t* a, uint32_t r, uint32_t s) {
+                 struct K : Fhp1Class { uint32_t solid; };
+                 K k;
+                 static_cast<Fhp1Class&>(k) = fhp1_classify(a, r, s);
+                 k.solid = s;
+                 return k;
+               },
+               [](const auto& k, uint32_t c, uint32_t r, const uint32_t* x_a, uint32_t* o, uint32_t& orr) {
+                 fhp1_apply(k, c, r, x_a, o, orr, k.solid);
+               });
   // chir_bit (fhpg_common.cuh) == bit 0 of fin64(z): random keys, and keys
   // whose low word is at the carry boundary.
   {
