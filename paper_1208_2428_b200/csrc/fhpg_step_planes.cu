@@ -96,6 +96,11 @@ struct PlaneRule<0> {
   }
 };
 // Warps per CTA (one CTA per SM): 16 with 2 words per lane, 8 with 4.
+// Programmatic dependent launch of the step kernels: the next step's grid is
+// launched while this one runs (griddepcontrol.wait orders its reads).
+#ifndef FHPG_PDL
+#define FHPG_PDL 1
+#endif
 #ifndef FHPG_STREAM_ONLY
 #define FHPG_STREAM_ONLY 0  // timing experiments (wrong results): 1 memory pipeline only,
                             // 2 loads only, 3 stores only, 4 loads + shared reads,
@@ -616,10 +621,17 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
     for (int k = 0; k < G::kSlots; ++k) mbar_init(bars + k * 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // Column keys from the step keys (independent of the previous step, so
+  // this overlaps its tail under PDL), then wait for the previous grid.
   for (int c = threadIdx.x; c < cta_cols; c += blockDim.x) {
-    sts64(kc_base + c * 8, a.zc[cta_x0 + c]);
-    if (FORCE) sts64(kf_base + c * 8, a.zf[cta_x0 + c]);
+    const uint64_t x = static_cast<uint64_t>(cta_x0 + c) + 1;
+    sts64(kc_base + c * 8, column_key(a.kc_cur, x));
+    if (FORCE) sts64(kf_base + c * 8, column_key(a.kf_cur, x));
   }
+#if FHPG_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   // Next step's column keys (read by the next launch only).
   if (a.zc_next) {
     const int n = gridDim.x * blockDim.x;
@@ -691,9 +703,6 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 // throughput, so each box carries several rows.
 #ifndef FHPG_BOX_ROWS
 #define FHPG_BOX_ROWS 4  // (2: 1972, 4: 1987-1995 GSUPS on cfg4)
-#endif
-#ifndef FHPG_PDL
-#define FHPG_PDL 1
 #endif
 #ifndef FHPG_EXTRA_CTAS
 #define FHPG_EXTRA_CTAS 1
@@ -1048,7 +1057,21 @@ void launch_nw(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = smem;
   }
+#if FHPG_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, step_planes_kernel<NW, FORCE, RULE>, a, maps[0], maps[1], maps[2]);
+#else
   step_planes_kernel<NW, FORCE, RULE><<<grid, kWarps * 32, smem, st>>>(a, maps[0], maps[1], maps[2]);
+#endif
 }
 
 // ---------------------------------------------------------------------------
