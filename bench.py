@@ -15,7 +15,12 @@ over ranks; `e2e` = the same metric through the reference-facing C-ABI call
 `case Backend::Cuda` shim of fhp::advance) with the copies inside the timed
 region. The reference arm times the reference library itself
 (oracle/_ref/libfhpref.so = /root/reference/proj/core compiled from source)
-through fhp::run_bench on the host cores.
+through fhp::run_bench on the host cores, on the same 16384 x 16384 lattice,
+loading the same FHP-III table from data/fhp3.fhptab with its own
+read_table_file; it imports nothing from this framework.
+
+`--gpus N` without torchrun re-executes itself under torch.distributed.run
+(one process per GPU, 127.0.0.1 rendezvous); rank 0 prints the line.
 """
 from __future__ import annotations
 
@@ -38,7 +43,9 @@ DENSITY = 0.2
 FORCE_P = 0.0
 BYTES_PER_SITE = 1.875  # 7 state bits read + 7 written + 1 obstacle bit
 METRIC = "FHP site updates/s (GSUPS) at 1/2/4/8 B200; fraction of HBM roofline"
-CPU_SAMPLE_ROWS = 2048  # reference CPU sample: 16384 x 2048 slab of the same workload
+TABLE_FILE = os.path.join(ROOT, "data", "fhp3.fhptab")  # FHPTAB01, `fhp_b200 tablegen --rules fhp3`
+CPU_DIGEST_STEPS = 10   # cpu_baseline: 1 warm-up + 10 timed steps of the full lattice
+MATRIX_ROWS = 256       # lanes x1 / scalar x1: a 16384 x 256 slab of the same workload
 
 
 def peaks():
@@ -116,41 +123,73 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def cpu_reference(W, H, steps, warmup, table, threads=None):
-    """fhp::run_bench(cfg) of the reference library on the host cores."""
-    from oracle.oracle import Ref  # checker / baseline only
-    ref = Ref()
-    res = ref.bench(W, H, steps, warmup, DENSITY, FORCE_P, SEED, table=table, backend="strips",
-                    threads=threads or os.cpu_count(), repeats=1)
-    return res
+def ref_lib():
+    from oracle.oracle import Ref  # checker / baseline only (never the measured product)
+    return Ref()
+
+
+def cpu_run(ref, W, H, steps, warmup, backend="strips", threads=None):
+    """fhp::run_bench(cfg) of the reference library on the host cores, the
+    FHP-III table read by the reference itself from the FHPTAB01 file."""
+    return ref.bench_file(W, H, steps, warmup, DENSITY, FORCE_P, SEED, table_file=TABLE_FILE,
+                          backend=backend, threads=threads, repeats=1)
+
+
+def cpu_matrix(ref):
+    """BASELINE.md's other CPU arms, lanes x1 and scalar x1, on a bounded slab."""
+    out = {}
+    for backend in ("lanes", "scalar"):
+        r = cpu_run(ref, W_LAT, MATRIX_ROWS, 3, 1, backend=backend, threads=1)
+        out[f"{backend}x1"] = {"value": r["mups"] / 1000.0, "unit": "GSUPS", "cores": 1,
+                               "sample": f"{W_LAT}x{MATRIX_ROWS} slab, 1 warmup + 3 timed steps"}
+    return out
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import paper_1208_2428_b200 as P
-    table = P.build_table("fhp3")
+    ref = ref_lib()
     threads = os.cpu_count()
-    res = cpu_reference(W_LAT, CPU_SAMPLE_ROWS, args.steps, args.warmup, table, threads)
+    W, H = W_LAT, H_PER_GPU
+    res = cpu_run(ref, W, H, args.steps, args.warmup, threads=threads)
     gsups = res["mups"] / 1000.0
-    sample = (f"{W_LAT}x{CPU_SAMPLE_ROWS} slab of the cfg4 workload (FHP-III, d=0.2, seed 4, "
-              f"p=0), fhp::run_bench strips x {threads} threads, {args.warmup} warmup + "
-              f"{args.steps} timed steps")
+    world = args.gpus
+    sample = (f"{W}x{H} lattice (cfg4, one GPU's share of cfg5 at N={world}), fhp::run_bench strips "
+              f"x {threads} threads, {args.warmup} warmup + {args.steps} timed steps, FHP-III read "
+              f"from data/fhp3.fhptab by the reference's read_table_file")
     line = {"metric": METRIC, "value": gsups, "unit": "GSUPS", "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": res["wall_seconds"] * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": "cfg4: FHP-III 16384x16384/GPU, x-periodic, walls rows 0/H-1, "
-                                   "d=0.2, seed 4, p=0 (CPU: bounded row slab)",
-                       "W": W_LAT, "H": CPU_SAMPLE_ROWS, "table": "FHP-III",
-                       "digest": f"{res['digest']:#018x}"},
+            "config": {"workload": "cfg4/cfg5: FHP-III 16384x16384 per GPU, x-periodic, walls "
+                                   "rows 0/H-1, d=0.2, seed 4, p=0",
+                       "W": W, "H": H, "table": "FHP-III (data/fhp3.fhptab)",
+                       "same_config": world == 1,
+                       "digest": f"{res['digest']:#018x}",
+                       "digest_after_steps": args.warmup + args.steps},
             "cpu_baseline": {"value": gsups, "unit": "GSUPS", "cores": threads,
                              "kind": "reference", "sample": sample},
+            "cpu_matrix": cpu_matrix(ref),
             "e2e": {"value": gsups, "unit": "GSUPS", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def spawn_ranks(args):
+    """`--gpus N` outside torchrun: re-run this script under
+    torch.distributed.run with N local ranks (rank 0 prints)."""
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -161,38 +200,45 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="print the launch plan (ranks, strips) and exit without a GPU")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    from paper_1208_2428_b200.strips import strip_rows
+    H = H_PER_GPU * world
+    rb, re = strip_rows(H, world)[rank]
+    if args.dry_run:
+        print(json.dumps({"dry_run": True, "rank": rank, "world": world, "local_rank": local,
+                          "W": W_LAT, "H": H, "rows": [rb, re]}), flush=True)
+        return 0
 
     import torch
     import torch.distributed as dist
 
     import paper_1208_2428_b200 as P
-    from paper_1208_2428_b200.strips import DistStrips, strip_rows
+    from paper_1208_2428_b200.strips import DistStrips
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N > 1 must be launched with torch.distributed.run")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
 
-    H = H_PER_GPU * world
-    rb, re = strip_rows(H, world)[rank]
     table = P.build_table("fhp3")
     eng = P.Engine(W_LAT, H, rb, re, local)
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    eng.set_stream(stream.cuda_stream)
     eng.set_table(table)
     eng.init(SEED, DENSITY)
     thr = P.bernoulli_threshold(FORCE_P)
-    strips = DistStrips(eng, rank, world)
+    strips = DistStrips(eng, rank, world)  # puts the engine on `stream` (NCCL's ordering stream)
 
     def barrier():
         if world > 1:
@@ -213,14 +259,14 @@ def main():
         torch.cuda.synchronize()
         barrier()
     ms = start.elapsed_time(end)
-    step_launches = eng.step_launches - launches0
-    # column-key launches: one per advance call
-    calls = args.steps if world > 1 else 1
-    gpu_launches = step_launches + calls
+    gpu_launches = eng.step_launches - launches0  # step kernels + column keys
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+        g = torch.tensor([gpu_launches], device="cuda", dtype=torch.int64)
+        dist.all_reduce(g)
+        gpu_launches = int(g.item())
     sites = W_LAT * H  # all ranks
     value = sites * args.steps / (ms * 1e-3) / 1e9
     ms_per_step = ms / args.steps
@@ -239,7 +285,7 @@ def main():
                                      "rows 0/H-1, d=0.2, seed 4, p=0; row strips across GPUs",
                          "W": W_LAT, "H": H, "rows_per_gpu": H_PER_GPU, "table": "FHP-III",
                          "parallelism": f"row-strips x{world}" if world > 1 else "single",
-                         "l2": "inputs larger than L2 (2 x 268 MB state buffers per GPU)",
+                         "l2": "inputs larger than L2 (2 x 272 MB state buffers per GPU)",
                          "kernel": {"planes": "bit-plane ring kernel (step_ring_kernel)",
                                     "bytes": "byte streaming kernel (step_fast_kernel)",
                                     "generic": "generic"}[eng.path]},
@@ -247,65 +293,102 @@ def main():
                            "frac": achieved / peak, "traffic": traffic,
                            "bytes_per_site": BYTES_PER_SITE, "peak_source": peak_src,
                            "timing": "CUDA events on the engine stream around the K-step loop, "
-                                     "per-step average (one step kernel per step)"},
+                                     "per-step average (one step kernel per step at N=1)"},
               "gpu_launches": gpu_launches,
               "clocks": clk.summary()}
-
-    # Parity stamp of the timed run: digest after warmup+K steps vs nothing (informational).
-    if rank == 0 and world == 1 and not args.no_e2e:
-        result["e2e"] = e2e_measure(P, table, args, thr)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count()
-        res = cpu_reference(W_LAT, CPU_SAMPLE_ROWS, 10, 1, table, threads)
-        result["cpu_baseline"] = {
-            "value": res["mups"] / 1000.0, "unit": "GSUPS", "cores": threads, "kind": "reference",
-            "sample": f"{W_LAT}x{CPU_SAMPLE_ROWS} slab of the same workload, fhp::run_bench "
-                      f"(oracle/_ref = reference proj/core built from source), strips x {threads} "
-                      f"threads, 1 warmup + 10 timed steps"}
+    if world == 1:
+        # Parity stamp: the state after warmup + K steps (compare with the
+        # reference arm's digest at the same step count).
+        result["config"]["digest"] = f"{P.state_digest(eng.download()):#018x}"
+        result["config"]["digest_after_steps"] = args.warmup + args.steps
     eng.close()
-    if rank == 0:
-        print(json.dumps(result), flush=True)
+    if not args.no_e2e:
+        e2e = e2e_measure(P, table, args, world, rank, rb, re, barrier)
+        if rank == 0:
+            result["e2e"] = e2e
+    barrier()
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(P, table, local)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
     return 0
 
 
-def e2e_measure(P, table, args, thr):
-    """fhp::advance through the C ABI on host buffers (the Backend::Cuda shim):
-    H2D of state + mask, K steps, D2H of the state, all inside the timed
-    region (wall clock around synchronous calls; pinned host memory)."""
+def cpu_baseline(P, table, device):
+    """The reference library on the host cores (all threads) on the full
+    16384^2 lattice for 1 + CPU_DIGEST_STEPS steps, and the same steps on the
+    GPU: the two digests must agree."""
     import torch
-    W, H = W_LAT, H_PER_GPU
-    src = P.Engine(W, H)
+    ref = ref_lib()
+    threads = os.cpu_count()
+    res = cpu_run(ref, W_LAT, H_PER_GPU, CPU_DIGEST_STEPS, 1, threads=threads)
+    e = P.Engine(W_LAT, H_PER_GPU, 0, H_PER_GPU, device)
+    e.set_table(table)
+    e.init(SEED, DENSITY)
+    e.advance(SEED, FORCE_P, 0, 1 + CPU_DIGEST_STEPS)
+    gpu_digest = P.state_digest(e.download())
+    e.close()
+    torch.cuda.synchronize()
+    return {"value": res["mups"] / 1000.0, "unit": "GSUPS", "cores": threads, "kind": "reference",
+            "sample": f"{W_LAT}x{H_PER_GPU} (the full per-GPU lattice), fhp::run_bench of "
+                      f"oracle/_ref (reference proj/core built from source), strips x {threads} "
+                      f"threads, 1 warmup + {CPU_DIGEST_STEPS} timed steps",
+            "digest": f"{res['digest']:#018x}", "gpu_digest": f"{gpu_digest:#018x}",
+            "digest_match": res["digest"] == gpu_digest}
+
+
+def e2e_measure(P, table, args, world, rank, rb, re, barrier):
+    """fhp::advance through the C ABI on host buffers (the Backend::Cuda shim
+    of INTEGRATION.md with a cached engine): H2D of state + obstacle mask
+    from pinned memory, K steps (halo exchange included at N > 1), D2H of the
+    state and the swap count, all inside the timed region; wall clock around
+    synchronous calls, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_1208_2428_b200.strips import DistStrips
+    W, rows = W_LAT, re - rb
+    src = P.Engine(W, world * H_PER_GPU, rb, re, torch.cuda.current_device())
     src.set_table(table)
     src.init(SEED, DENSITY)
-    host = torch.empty((H, W), dtype=torch.uint8, pin_memory=True).numpy()
+    host = torch.empty((rows, W), dtype=torch.uint8, pin_memory=True).numpy()
     src.download(host)
-    mask = torch.empty((H, W), dtype=torch.uint8, pin_memory=True).numpy()
+    mask = torch.empty((rows, W), dtype=torch.uint8, pin_memory=True).numpy()
     np.right_shift(host, 7, out=mask)
     src.close()
-    e = P.Engine(W, H)
+    e = P.Engine(W, world * H_PER_GPU, rb, re, torch.cuda.current_device())
     e.set_table(table)
+    strips = DistStrips(e, rank, world)
+    thr = P.bernoulli_threshold(FORCE_P)
     # warm-up of the path
     e.set_obstacles(mask)
     e.upload(host)
-    e.advance(SEED, FORCE_P, 0, 3)
+    strips.advance(SEED, thr, 0, 3)
     torch.cuda.synchronize()
-    out = torch.empty((H, W), dtype=torch.uint8, pin_memory=True).numpy()
+    out = torch.empty((rows, W), dtype=torch.uint8, pin_memory=True).numpy()
+    barrier()
     t0 = time.perf_counter()
     e.set_obstacles(mask)
     e.upload(host)
-    e.advance(SEED, FORCE_P, args.warmup, args.steps)
+    strips.advance(SEED, thr, args.warmup, args.steps)
     e.download(out)
     t1 = time.perf_counter()
     e.close()
     secs = t1 - t0
-    h2d = 2 * W * H  # state + obstacle mask
-    d2h = W * H + 8  # state + swap count
-    return {"value": W * H * args.steps / secs / 1e9, "unit": "GSUPS",
-            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
-            "call": f"fhpg_set_obstacles+fhpg_upload+fhpg_advance({args.steps} steps)+fhpg_download "
-                    "on pinned host buffers", "seconds": secs}
+    if world > 1:
+        t = torch.tensor([secs], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        secs = float(t.item())
+    h2d = 2 * W * rows  # state + obstacle mask (per rank)
+    d2h = W * rows + 8  # state + swap count
+    return {"value": W * world * H_PER_GPU * args.steps / secs / 1e9, "unit": "GSUPS",
+            "h2d_bytes_per_step": world * h2d / args.steps,
+            "d2h_bytes_per_step": world * d2h / args.steps,
+            "call": f"fhpg_set_obstacles+fhpg_upload+fhpg_advance({args.steps} steps)+"
+                    "fhpg_download on pinned host buffers"
+                    + (" per rank, halo exchange over NCCL" if world > 1 else ""),
+            "seconds": secs}
 
 
 if __name__ == "__main__":

@@ -56,6 +56,27 @@ int fhpg_create(int width, int height, fhpg_engine** out);
 int fhpg_create_strip(int width, int height, int row_begin, int row_end, int device,
                       fhpg_engine** out);
 
+/* Engine for a whole W x H lattice split into n_strips row strips, strip i on
+ * CUDA device devices[i] (devices == NULL: device i; several strips may share
+ * a device). Rows follow make_strip_plan + worker_rows (backends.cpp:20-36,
+ * 140-145): balanced interior strips, strip 0 also owns wall row 0 and the
+ * last strip row H-1; n_strips > H-2 is FHPG_EINVAL with the reference's
+ * message. The engine owns every strip's buffers and streams and runs the
+ * halo exchange itself (peer copies over NVLink between neighbouring strips,
+ * overlapped with the interior rows of each step): every call below works on
+ * it as on a single-device engine over the whole lattice (uploads, masks and
+ * downloads cover all H rows; observables and swaps are summed over the
+ * strips), except fhpg_set_stream, fhpg_advance_part and fhpg_halo
+ * (FHPG_EINVAL: the engine orders its strips' streams itself). This is the
+ * `gpus` of fhp_b200::SimConfig. */
+int fhpg_create_multi(int width, int height, int n_strips, const int* devices,
+                      fhpg_engine** out);
+
+/* Strip layout of an engine: *n_strips (1 for a single-strip engine) and,
+ * for each strip i (arrays of n_strips entries, each may be NULL), its rows
+ * [row_begin[i], row_end[i]) and CUDA device. */
+int fhpg_strips(fhpg_engine* e, int* n_strips, int* row_begin, int* row_end, int* device);
+
 void fhpg_destroy(fhpg_engine* e);
 
 /* Thread-local message of the last failure ("" if none). */
@@ -142,7 +163,8 @@ int fhpg_halo(fhpg_engine* e, void** send_top, void** send_bottom, void** recv_t
 
 /* Introspection: W, H, row_begin, row_end, which step kernel runs
  * (2 = bit-plane path, 1 = byte streaming path, 0 = generic), and the number
- * of step-kernel launches enqueued so far. */
+ * of kernels the stepping has enqueued so far (step kernels, the per-call
+ * column keys, bit-7 normalisation). */
 int fhpg_info(fhpg_engine* e, int* width, int* height, int* row_begin, int* row_end,
               int* fast_path, uint64_t* step_launches);
 

@@ -192,6 +192,9 @@ class Ref:
         L.ref_velocity_profile.argtypes = [C.c_int, C.c_int, u8p, f64p, i32p]
         L.ref_bench.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                 C.c_uint64, C.c_int, C.c_int, u8p, C.c_int, f64p, f64p, u64p]
+        L.ref_bench_file.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                     C.c_uint64, C.c_int, C.c_int, C.c_char_p, C.c_int, f64p,
+                                     f64p, u64p]
 
     def _check(self, rc):
         if rc != 0:
@@ -288,6 +291,19 @@ class Ref:
         self._check(self.lib.ref_bench(W, H, steps, warmup, density, force_p, seed,
                                        BACKENDS[backend], threads, _ptr(t), repeats,
                                        C.byref(mups), C.byref(secs), C.byref(dg)))
+        return dict(mups=mups.value, wall_seconds=secs.value, digest=dg.value, threads=threads)
+
+
+    def bench_file(self, W, H, steps, warmup, density, force_p, seed, table_file=None,
+                   backend="strips", threads=None, repeats=1):
+        """run_bench with cfg.table_file: the reference loads the FHPTAB01 file itself."""
+        if threads is None:
+            threads = max(1, min(os.cpu_count() or 1, H - 2)) if backend in ("strips", "tiles") else 1
+        mups, secs, dg = C.c_double(), C.c_double(), C.c_uint64()
+        path = None if table_file is None else os.fsencode(table_file)
+        self._check(self.lib.ref_bench_file(W, H, steps, warmup, density, force_p, seed,
+                                            BACKENDS[backend], threads, path, repeats,
+                                            C.byref(mups), C.byref(secs), C.byref(dg)))
         return dict(mups=mups.value, wall_seconds=secs.value, digest=dg.value, threads=threads)
 
 

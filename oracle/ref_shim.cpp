@@ -285,4 +285,35 @@ int ref_bench(int W, int H, int steps, int warmup, double density, double force_
   }
 }
 
+// fhp::run_bench(cfg, repeats) with cfg.table_file = an FHPTAB01 file (the
+// reference's own read_table_file / load_table, collision.cpp:137-170, reads
+// it; nullptr = the DEFAULT table).
+int ref_bench_file(int W, int H, int steps, int warmup, double density, double force_p,
+                   uint64_t seed, int backend, int threads, const char* table_file,
+                   int repeats, double* mups, double* wall_seconds, uint64_t* digest) {
+  try {
+    fhp::SimConfig cfg;
+    cfg.width = W;
+    cfg.height = H;
+    cfg.steps = steps;
+    cfg.warmup_steps = warmup;
+    cfg.fill_density = density;
+    cfg.force_p = force_p;
+    cfg.seed = seed;
+    cfg.backend = backend_of(backend);
+    cfg.threads = threads;
+    cfg.lanes = 64;
+    if (table_file) cfg.table_file = table_file;
+    const auto res = fhp::run_bench(cfg, repeats);
+    *mups = res.median.mups;
+    *wall_seconds = res.median.wall_seconds;
+    *digest = res.median.state_digest;
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    return fail(e, 2);
+  } catch (const std::exception& e) {
+    return fail(e, 3);
+  }
+}
+
 }  // extern "C"

@@ -67,7 +67,10 @@ def parse(data: bytes, verify: bool = True) -> Checkpoint:
 
 
 def capture(engine, next_step: int, seed: int, force_p: float, swaps: int, table) -> Checkpoint:
-    """Download a whole-lattice engine into a Checkpoint record."""
+    """Download a whole-lattice engine into a Checkpoint record (a strip
+    engine holds only part of the lattice: rejected, as in checkpoint.cpp)."""
+    if getattr(engine, "nrows", None) is not None and engine.nrows != engine.H:
+        raise ValueError("checkpoint: engine holds a row strip, not the whole lattice")
     state = engine.download()
     H, W = state.shape
     return Checkpoint(W, H, int(next_step), int(seed), float(force_p), int(swaps),
@@ -76,6 +79,8 @@ def capture(engine, next_step: int, seed: int, force_p: float, swaps: int, table
 
 def restore(engine, ck: Checkpoint) -> None:
     """Table, obstacles (bit 7) and state back into an engine of the same size."""
+    if getattr(engine, "nrows", None) is not None and (engine.nrows, engine.W) != (ck.H, ck.W):
+        raise ValueError("checkpoint: engine size differs from the checkpoint's lattice")
     engine.set_table(ck.table)
     engine.set_obstacles((ck.state >> 7).astype(np.uint8))
     engine.upload(ck.state)

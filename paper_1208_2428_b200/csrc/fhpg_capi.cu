@@ -1,5 +1,6 @@
 // fhpg_capi.cu — the C ABI (include/fhpg.h): engine object, device memory,
 // error mapping, and the step loop that drives the kernels.
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -7,6 +8,7 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/fhpg.h"
 #include "../../include/fhpg_tables.h"
@@ -36,14 +38,24 @@ struct fhpg_engine {
   long long* acc = nullptr;              // reduction scratch (3)
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
+  cudaEvent_t tail = nullptr;            // recorded after the last enqueued work (any stream)
   bool table_set = false;
   bool normalized = true;                // state bit 7 == mask
   int num_sms = 148;
-  uint64_t launches = 0;
+  uint64_t launches = 0;                 // kernels enqueued by stepping (step, keys, mask)
   int64_t keys_step = -1;                // step whose column keys are in keys(step & 1)
   uint64_t keys_seed = 0;
   bool keys_force = false;
 
+  // Multi-strip engine (fhpg_create_multi): the strips, one engine each (on
+  // its own device and stream), and the halo-exchange machinery. Empty for
+  // a single-strip engine.
+  std::vector<fhpg_engine*> parts;
+  std::vector<cudaStream_t> halo_stream;   // per strip: the halo copies into it
+  std::vector<cudaEvent_t> ev_done;        // per strip: its last step's boundary rows are done
+  std::vector<cudaEvent_t> ev_halo;        // per strip: its halos for this step have landed
+
+  bool multi() const { return !parts.empty(); }
   uint8_t* base(int which) const { return buf[which] + pitch; }  // local row 0
   uint64_t* keys(int parity, int purpose) const {
     return zkeys + (static_cast<size_t>(parity) * 2 + purpose) * static_cast<size_t>(W);
@@ -106,6 +118,17 @@ void need(const fhpg_engine* e) {
 
 void release(fhpg_engine* e) {
   if (!e) return;
+  for (size_t i = 0; i < e->parts.size(); ++i) {
+    cudaSetDevice(e->parts[i]->device);
+    if (i < e->halo_stream.size() && e->halo_stream[i]) cudaStreamDestroy(e->halo_stream[i]);
+    if (i < e->ev_done.size() && e->ev_done[i]) cudaEventDestroy(e->ev_done[i]);
+    if (i < e->ev_halo.size() && e->ev_halo[i]) cudaEventDestroy(e->ev_halo[i]);
+    release(e->parts[i]);
+  }
+  if (e->multi()) {
+    delete e;
+    return;
+  }
   cudaFree(e->buf[0]);
   cudaFree(e->buf[1]);
   cudaFree(e->mask);
@@ -115,6 +138,7 @@ void release(fhpg_engine* e) {
   cudaFree(e->swaps);
   cudaFree(e->acc);
   if (e->own_stream) cudaStreamDestroy(e->own_stream);
+  if (e->tail) cudaEventDestroy(e->tail);
   delete e;
 }
 
@@ -157,6 +181,7 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
     ck(cudaMalloc(&e->acc, sizeof(long long) * 4), "cudaMalloc(acc)");
     ck(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     e->stream = e->own_stream;
+    ck(cudaEventCreateWithFlags(&e->tail, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device),
        "cudaDeviceGetAttribute");
     ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
@@ -242,6 +267,7 @@ void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64
   if (!e->planes && !e->normalized) {
     launch_apply_mask(e->base(e->cur), e->mask, e->pitch, e->W, e->nrows, st);
     ck(cudaGetLastError(), "apply_mask launch");
+    ++e->launches;
     e->normalized = true;
   }
   const bool force = thr != 0;
@@ -249,6 +275,7 @@ void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64
   launch_column_keys(e->keys(s0 & 1, 0), force ? e->keys(s0 & 1, 1) : nullptr,
                      step_key(seed, kChirality, s0), step_key(seed, kForcing, s0), e->W, st);
   ck(cudaGetLastError(), "column_keys launch");
+  ++e->launches;
   for (int64_t i = 0; i < count; ++i) {
     const uint64_t s = static_cast<uint64_t>(first + i);
     StepArgs a{};
@@ -278,6 +305,7 @@ void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64
     e->cur ^= 1;
   }
   e->keys_step = -1;
+  ck(cudaEventRecord(e->tail, st), "cudaEventRecord");
 }
 
 // One step in two parts for strips that overlap the halo exchange with the
@@ -292,6 +320,7 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
   if (!e->planes && !e->normalized) {
     launch_apply_mask(e->base(e->cur), e->mask, e->pitch, e->W, e->nrows, st);
     ck(cudaGetLastError(), "apply_mask launch");
+    ++e->launches;
     e->normalized = true;
   }
   const bool force = thr != 0;
@@ -300,6 +329,7 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
     launch_column_keys(e->keys(s & 1, 0), force ? e->keys(s & 1, 1) : nullptr,
                        step_key(seed, kChirality, s), step_key(seed, kForcing, s), e->W, st);
     ck(cudaGetLastError(), "column_keys launch");
+    ++e->launches;
     e->keys_step = step;
     e->keys_seed = seed;
     e->keys_force = force;
@@ -334,6 +364,7 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
   };
   if (part == 0) {
     if (interior) run(1, e->nrows - 1, true);
+    ck(cudaEventRecord(e->tail, st), "cudaEventRecord");
     return;
   }
   if (interior && e->planes) {
@@ -352,12 +383,186 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
   }
   e->cur ^= 1;
   e->keys_step = step + 1;  // computed by part 0 (or by the single launch above)
+  ck(cudaEventRecord(e->tail, st), "cudaEventRecord");
 }
 
 void copy_rows_h2d(uint8_t* dev, size_t pitch, const uint8_t* host, size_t stride, int W,
                    int rows, cudaStream_t st) {
   ck(cudaMemcpy2DAsync(dev, pitch, host, stride, W, rows, cudaMemcpyHostToDevice, st),
      "cudaMemcpy2D H2D");
+}
+
+// ---------------------------------------------------------------------------
+// Multi-strip engine: the device analog of the strips backend (make_strip_plan
+// backends.cpp:20-36, worker_rows :140-145, run_strips :149-219) with one
+// strip per GPU. Per step and strip j (stream S_j, halo stream T_j):
+//   T_j: wait done(j-1), done(j), done(j+1) of the previous step, copy the
+//        neighbours' boundary rows into j's halo rows (peer copies over
+//        NVLink when the strips sit on different GPUs), record halo(j);
+//   S_j: interior rows (no halo needed; overlaps the copies), wait halo(j),
+//        boundary rows + buffer swap, record done(j).
+// The waits order every read of a boundary row after the step that wrote
+// it, and every overwrite of a halo row or boundary row after the last read
+// of its previous contents (the neighbour's boundary launch of the step
+// before). Every random decision is keyed by global (x, y, step), so the
+// strips reproduce the single-engine bits exactly.
+// ---------------------------------------------------------------------------
+std::vector<std::pair<int, int>> strip_plan(int H, int n) {
+  // make_strip_plan (same messages) + worker_rows: strip 0 also owns wall
+  // row 0, the last strip wall row H-1.
+  const int interior = H - 2;
+  if (n < 1) invalid("strip count must be >= 1");
+  if (n > interior) invalid("strip count exceeds interior row count");
+  std::vector<std::pair<int, int>> rows;
+  const int base = interior / n, extra = interior % n;
+  int r = 1;
+  for (int i = 0; i < n; ++i) {
+    const int k = base + (i < extra ? 1 : 0);
+    rows.emplace_back(r, r + k);
+    r += k;
+  }
+  rows.front().first = 0;
+  rows.back().second = H;
+  return rows;
+}
+
+void create_multi(int W, int H, int n, const int* devices, fhpg_engine** out) {
+  if (!out) invalid("null output pointer");
+  *out = nullptr;
+  if (W < 1) invalid("lattice width must be >= 1");
+  if (H < 3) invalid("lattice height must be >= 3");
+  const auto plan = strip_plan(H, n);
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  std::vector<int> dev(n);
+  for (int i = 0; i < n; ++i) {
+    dev[i] = devices ? devices[i] : i;
+    if (dev[i] < 0 || dev[i] >= ndev) invalid("CUDA device index out of range");
+  }
+  auto* m = new fhpg_engine;
+  m->W = W;
+  m->H = H;
+  m->row_begin = 0;
+  m->row_end = H;
+  m->nrows = H;
+  m->device = dev[0];
+  try {
+    for (int i = 0; i < n; ++i) {
+      fhpg_engine* p = nullptr;
+      create(W, H, plan[i].first, plan[i].second, dev[i], &p);
+      m->parts.push_back(p);
+      DeviceGuard g(dev[i]);
+      cudaStream_t hs = nullptr;
+      cudaEvent_t d = nullptr, h = nullptr;
+      ck(cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking), "cudaStreamCreate(halo)");
+      m->halo_stream.push_back(hs);
+      ck(cudaEventCreateWithFlags(&d, cudaEventDisableTiming), "cudaEventCreate");
+      m->ev_done.push_back(d);
+      ck(cudaEventCreateWithFlags(&h, cudaEventDisableTiming), "cudaEventCreate");
+      m->ev_halo.push_back(h);
+    }
+    // Peer access between neighbouring strips on different GPUs (NVLink).
+    for (int i = 0; i + 1 < n; ++i) {
+      if (dev[i] == dev[i + 1]) continue;
+      for (const auto& pr : {std::make_pair(dev[i], dev[i + 1]), std::make_pair(dev[i + 1], dev[i])}) {
+        int can = 0;
+        ck(cudaDeviceCanAccessPeer(&can, pr.first, pr.second), "cudaDeviceCanAccessPeer");
+        if (!can) continue;  // cudaMemcpyPeerAsync still works, staged by the driver
+        DeviceGuard g(pr.first);
+        const cudaError_t err = cudaDeviceEnablePeerAccess(pr.second, 0);
+        if (err == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else ck(err, "cudaDeviceEnablePeerAccess");
+      }
+    }
+  } catch (...) {
+    release(m);
+    throw;
+  }
+  *out = m;
+}
+
+struct Halo {
+  uint8_t *send_top, *send_bottom, *recv_top, *recv_bottom;
+  size_t row_bytes;
+};
+Halo halo_of(fhpg_engine* e) {
+  uint8_t* b = e->base(e->cur);
+  return {b, b + static_cast<size_t>(e->nrows - 1) * e->pitch, b - e->pitch,
+          b + static_cast<size_t>(e->nrows) * e->pitch,
+          e->planes ? fhpg::planes_row_bytes(e->W) : static_cast<size_t>(e->W)};
+}
+
+void multi_step_loop(fhpg_engine* m, uint64_t seed, uint64_t thr, int64_t first, int64_t count) {
+  const int n = static_cast<int>(m->parts.size());
+  auto& P = m->parts;
+  if (n == 1) {
+    DeviceGuard g(P[0]->device);
+    step_loop(P[0], seed, thr, first, count);
+    return;
+  }
+  nvtxRangePushA("fhpg.advance(multi)");
+  for (int j = 0; j < n; ++j) {  // the work already enqueued on every strip
+    DeviceGuard g(P[j]->device);
+    ck(cudaEventRecord(m->ev_done[j], P[j]->stream), "cudaEventRecord");
+  }
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t s = first + i;
+    nvtxRangePushA("fhpg.step");
+    nvtxRangePushA("fhpg.halo");
+    for (int j = 0; j < n; ++j) {
+      DeviceGuard g(P[j]->device);
+      const cudaStream_t hs = m->halo_stream[j];
+      for (int k = std::max(0, j - 1); k <= std::min(n - 1, j + 1); ++k)
+        ck(cudaStreamWaitEvent(hs, m->ev_done[k], 0), "cudaStreamWaitEvent");
+      const Halo me = halo_of(P[j]);
+      if (j > 0) {
+        const Halo up = halo_of(P[j - 1]);
+        ck(cudaMemcpyPeerAsync(me.recv_top, P[j]->device, up.send_bottom, P[j - 1]->device,
+                               me.row_bytes, hs), "halo copy (top)");
+      }
+      if (j + 1 < n) {
+        const Halo dn = halo_of(P[j + 1]);
+        ck(cudaMemcpyPeerAsync(me.recv_bottom, P[j]->device, dn.send_top, P[j + 1]->device,
+                               me.row_bytes, hs), "halo copy (bottom)");
+      }
+      ck(cudaEventRecord(m->ev_halo[j], hs), "cudaEventRecord");
+    }
+    nvtxRangePop();
+    nvtxRangePushA("fhpg.interior");
+    for (int j = 0; j < n; ++j) {
+      DeviceGuard g(P[j]->device);
+      step_part(P[j], seed, thr, s, 0);
+    }
+    nvtxRangePop();
+    nvtxRangePushA("fhpg.boundary");
+    for (int j = 0; j < n; ++j) {
+      DeviceGuard g(P[j]->device);
+      ck(cudaStreamWaitEvent(P[j]->stream, m->ev_halo[j], 0), "cudaStreamWaitEvent");
+      step_part(P[j], seed, thr, s, 1);
+      ck(cudaEventRecord(m->ev_done[j], P[j]->stream), "cudaEventRecord");
+    }
+    nvtxRangePop();
+    nvtxRangePop();
+  }
+  nvtxRangePop();
+}
+
+// Apply fn to every strip of a multi engine (on its device), or to e itself.
+template <typename F>
+void each(fhpg_engine* e, F&& fn) {
+  if (!e->multi()) {
+    DeviceGuard g(e->device);
+    fn(e);
+    return;
+  }
+  for (fhpg_engine* p : e->parts) {
+    DeviceGuard g(p->device);
+    fn(p);
+  }
+}
+
+void single_only(const fhpg_engine* e, const char* what) {
+  if (e->multi()) invalid(std::string(what) + " is not available on a multi-strip engine");
 }
 
 }  // namespace
@@ -387,12 +592,24 @@ int fhpg_create_strip(int width, int height, int row_begin, int row_end, int dev
   return guarded([&] { create(width, height, row_begin, row_end, device, out); });
 }
 
+int fhpg_create_multi(int width, int height, int n_strips, const int* devices,
+                      fhpg_engine** out) {
+  return guarded([&] { create_multi(width, height, n_strips, devices, out); });
+}
+
 void fhpg_destroy(fhpg_engine* e) {
   if (!e) return;
   int prev = 0;
   cudaGetDevice(&prev);
-  cudaSetDevice(e->device);
-  cudaStreamSynchronize(e->stream);
+  each(e, [](fhpg_engine* p) {
+    // The tail event, not the stream: a caller stream set with
+    // fhpg_set_stream may already be gone.
+    cudaEventSynchronize(p->tail);
+  });
+  for (size_t i = 0; i < e->halo_stream.size(); ++i) {
+    cudaSetDevice(e->parts[i]->device);
+    cudaStreamSynchronize(e->halo_stream[i]);
+  }
   release(e);
   cudaSetDevice(prev);
 }
@@ -400,7 +617,14 @@ void fhpg_destroy(fhpg_engine* e) {
 int fhpg_set_stream(fhpg_engine* e, void* s) {
   return guarded([&] {
     need(e);
-    e->stream = static_cast<cudaStream_t>(s);  // NULL = the legacy default stream
+    single_only(e, "fhpg_set_stream");
+    DeviceGuard g(e->device);
+    // Work already enqueued on the old stream (PDL step kernels run
+    // asynchronously) is ordered before anything enqueued on the new one.
+    ck(cudaEventRecord(e->tail, e->stream), "cudaEventRecord");
+    const cudaStream_t ns = static_cast<cudaStream_t>(s);  // NULL = the legacy default stream
+    ck(cudaStreamWaitEvent(ns, e->tail, 0), "cudaStreamWaitEvent");
+    e->stream = ns;
   });
 }
 
@@ -409,25 +633,31 @@ int fhpg_set_table(fhpg_engine* e, const uint8_t* t) {
     need(e);
     if (!t) invalid("null table");
     for (int i = 0; i < 512; ++i)
-      if ((t[i] & 0x80u) != (i & 0x80)) invalid("collision table: entry " + std::to_string(i) + " changes the obstacle bit");
-    DeviceGuard g(e->device);
-    ck(cudaMemcpyAsync(e->table, t, 512, cudaMemcpyHostToDevice, e->stream), "table upload");
-    ck(cudaStreamSynchronize(e->stream), "table upload sync");
-    e->table_set = true;
+      if ((t[i] & 0x80u) != (i & 0x80))
+        invalid("collision table: entry " + std::to_string(i) + " changes the obstacle bit");
     // The bit-plane kernels evaluate FHP-III, FHP-I and the reference's
     // DEFAULT rule as circuits (fhpg_planes_rules.cuh); any other table runs
     // the byte LUT path.
-    e->table_planes = false;
+    bool planes = false;
+    int rule = 2;
     for (const int v : {FHPG_RULES_FHP_III, FHPG_RULES_FHP_I, FHPG_RULES_DEFAULT}) {
       uint8_t ref[512];
       fhpg_build_table(v, ref);
       if (std::memcmp(t, ref, 512) == 0) {
-        e->table_planes = true;
-        e->planes_rule = v;
+        planes = true;
+        rule = v;
         break;
       }
     }
-    sync_layout(e);
+    each(e, [&](fhpg_engine* p) {
+      ck(cudaMemcpyAsync(p->table, t, 512, cudaMemcpyHostToDevice, p->stream), "table upload");
+      ck(cudaStreamSynchronize(p->stream), "table upload sync");
+      p->table_set = true;
+      p->table_planes = planes;
+      p->planes_rule = rule;
+      sync_layout(p);
+    });
+    e->table_set = true;
   });
 }
 
@@ -436,15 +666,17 @@ int fhpg_set_obstacles(fhpg_engine* e, const uint8_t* mask, size_t stride) {
     need(e);
     if (!mask) invalid("null mask");
     if (stride < static_cast<size_t>(e->W)) invalid("stride < width");
-    DeviceGuard g(e->device);
-    // Raw bytes (nonzero = solid) go straight to the device mask.
-    copy_rows_h2d(e->mask, e->pitch, mask, stride, e->W, e->nrows, e->stream);
-    // Lattice::set_obstacle also sets / clears bit 7 of the node (lattice.cpp:25-29).
-    uint8_t* v = bytes_view(e);
-    fhpg::launch_apply_mask(v, e->mask, e->pitch, e->W, e->nrows, e->stream);
-    ck(cudaGetLastError(), "apply_mask launch");
-    if (e->planes) pack_from_scratch(e);
-    ck(cudaStreamSynchronize(e->stream), "mask sync");
+    each(e, [&](fhpg_engine* p) {
+      // Raw bytes (nonzero = solid) go straight to the device mask.
+      copy_rows_h2d(p->mask, p->pitch, mask + static_cast<size_t>(p->row_begin - e->row_begin) * stride, stride,
+                    p->W, p->nrows, p->stream);
+      // Lattice::set_obstacle also sets / clears bit 7 of the node (lattice.cpp:25-29).
+      uint8_t* v = bytes_view(p);
+      fhpg::launch_apply_mask(v, p->mask, p->pitch, p->W, p->nrows, p->stream);
+      ck(cudaGetLastError(), "apply_mask launch");
+      if (p->planes) pack_from_scratch(p);
+      ck(cudaStreamSynchronize(p->stream), "mask sync");
+    });
   });
 }
 
@@ -453,19 +685,21 @@ int fhpg_upload(fhpg_engine* e, const uint8_t* state, size_t stride) {
     need(e);
     if (!state) invalid("null state");
     if (stride < static_cast<size_t>(e->W)) invalid("stride < width");
-    DeviceGuard g(e->device);
-    if (e->planes) {
-      // The byte image stays exact until the first step; the planes take
-      // bit 7 from the mask like the reference's motion pass.
-      need_scratch(e);
-      copy_rows_h2d(e->scratch, e->pitch, state, stride, e->W, e->nrows, e->stream);
-      e->scratch_valid = true;
-      pack_from_scratch(e);
-    } else {
-      copy_rows_h2d(e->base(e->cur), e->pitch, state, stride, e->W, e->nrows, e->stream);
-      e->normalized = false;
-    }
-    ck(cudaStreamSynchronize(e->stream), "upload sync");
+    each(e, [&](fhpg_engine* p) {
+      const uint8_t* src = state + static_cast<size_t>(p->row_begin - e->row_begin) * stride;
+      if (p->planes) {
+        // The byte image stays exact until the first step; the planes take
+        // bit 7 from the mask like the reference's motion pass.
+        need_scratch(p);
+        copy_rows_h2d(p->scratch, p->pitch, src, stride, p->W, p->nrows, p->stream);
+        p->scratch_valid = true;
+        pack_from_scratch(p);
+      } else {
+        copy_rows_h2d(p->base(p->cur), p->pitch, src, stride, p->W, p->nrows, p->stream);
+        p->normalized = false;
+      }
+    });
+    each(e, [&](fhpg_engine* p) { ck(cudaStreamSynchronize(p->stream), "upload sync"); });
   });
 }
 
@@ -474,11 +708,13 @@ int fhpg_download(fhpg_engine* e, uint8_t* state, size_t stride) {
     need(e);
     if (!state) invalid("null state");
     if (stride < static_cast<size_t>(e->W)) invalid("stride < width");
-    DeviceGuard g(e->device);
-    ck(cudaMemcpy2DAsync(state, stride, bytes_view(e), e->pitch, e->W, e->nrows,
-                         cudaMemcpyDeviceToHost, e->stream),
-       "cudaMemcpy2D D2H");
-    ck(cudaStreamSynchronize(e->stream), "download sync");
+    each(e, [&](fhpg_engine* p) {
+      ck(cudaMemcpy2DAsync(state + static_cast<size_t>(p->row_begin - e->row_begin) * stride,
+                           stride, bytes_view(p), p->pitch, p->W, p->nrows,
+                           cudaMemcpyDeviceToHost, p->stream),
+         "cudaMemcpy2D D2H");
+    });
+    each(e, [&](fhpg_engine* p) { ck(cudaStreamSynchronize(p->stream), "download sync"); });
   });
 }
 
@@ -487,25 +723,26 @@ int fhpg_init(fhpg_engine* e, uint64_t seed, double fill_density) {
     need(e);
     // lattice.cpp:58-60
     if (!(fill_density >= 0.0 && fill_density <= 1.0)) invalid("fill_density must be in [0,1]");
-    DeviceGuard g(e->device);
-    if (e->planes) need_scratch(e);
-    uint8_t* target = e->planes ? e->scratch : e->base(e->cur);
-    fhpg::launch_init(target, e->mask, e->pitch, e->W, e->nrows, e->row_begin, e->H,
-                      seed, fhpg::bernoulli_threshold(fill_density), e->stream);
-    ck(cudaGetLastError(), "init launch");
-    // Walls join the obstacle mask (init_impl calls set_obstacle on them).
-    for (int r = 0; r < e->nrows; ++r) {
-      const long long gr = e->row_begin + r;
-      if (gr == 0 || gr == e->H - 1)
-        ck(cudaMemsetAsync(e->mask + static_cast<size_t>(r) * e->pitch, 1, e->W, e->stream),
-           "wall mask");
-    }
-    if (e->planes) {
-      e->scratch_valid = true;
-      pack_from_scratch(e);
-    }
-    ck(cudaStreamSynchronize(e->stream), "init sync");
-    e->normalized = true;
+    each(e, [&](fhpg_engine* p) {
+      if (p->planes) need_scratch(p);
+      uint8_t* target = p->planes ? p->scratch : p->base(p->cur);
+      fhpg::launch_init(target, p->mask, p->pitch, p->W, p->nrows, p->row_begin, p->H, seed,
+                        fhpg::bernoulli_threshold(fill_density), p->stream);
+      ck(cudaGetLastError(), "init launch");
+      // Walls join the obstacle mask (init_impl calls set_obstacle on them).
+      for (int r = 0; r < p->nrows; ++r) {
+        const long long gr = p->row_begin + r;
+        if (gr == 0 || gr == p->H - 1)
+          ck(cudaMemsetAsync(p->mask + static_cast<size_t>(r) * p->pitch, 1, p->W, p->stream),
+             "wall mask");
+      }
+      if (p->planes) {
+        p->scratch_valid = true;
+        pack_from_scratch(p);
+      }
+      p->normalized = true;
+    });
+    each(e, [&](fhpg_engine* p) { ck(cudaStreamSynchronize(p->stream), "init sync"); });
   });
 }
 
@@ -513,6 +750,10 @@ int fhpg_advance_async(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t firs
   return guarded([&] {
     need(e);
     if (count <= 0) return;  // backends.cpp:157 — no-op, state untouched
+    if (e->multi()) {
+      multi_step_loop(e, seed, thr, first, count);
+      return;
+    }
     DeviceGuard g(e->device);
     step_loop(e, seed, thr, first, count);
   });
@@ -524,19 +765,30 @@ int fhpg_advance(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int
     need(e);
     if (swaps) *swaps = 0;
     if (count <= 0) return;
-    DeviceGuard g(e->device);
-    ck(cudaMemsetAsync(e->swaps, 0, sizeof(unsigned long long), e->stream), "swap reset");
-    step_loop(e, seed, thr, first, count);
-    unsigned long long s = 0;
-    ck(cudaMemcpyAsync(&s, e->swaps, sizeof s, cudaMemcpyDeviceToHost, e->stream), "swap read");
-    ck(cudaStreamSynchronize(e->stream), "advance sync");
-    if (swaps) *swaps = s;
+    each(e, [&](fhpg_engine* p) {
+      ck(cudaMemsetAsync(p->swaps, 0, sizeof(unsigned long long), p->stream), "swap reset");
+    });
+    if (e->multi()) {
+      multi_step_loop(e, seed, thr, first, count);
+    } else {
+      DeviceGuard g(e->device);
+      step_loop(e, seed, thr, first, count);
+    }
+    unsigned long long total = 0;
+    each(e, [&](fhpg_engine* p) {
+      unsigned long long s = 0;
+      ck(cudaMemcpyAsync(&s, p->swaps, sizeof s, cudaMemcpyDeviceToHost, p->stream), "swap read");
+      ck(cudaStreamSynchronize(p->stream), "advance sync");
+      total += s;
+    });
+    if (swaps) *swaps = total;
   });
 }
 
 int fhpg_advance_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int part) {
   return guarded([&] {
     need(e);
+    single_only(e, "fhpg_advance_part");
     DeviceGuard g(e->device);
     step_part(e, seed, thr, step, part);
   });
@@ -545,36 +797,41 @@ int fhpg_advance_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step,
 int fhpg_swaps(fhpg_engine* e, uint64_t* swaps, int reset) {
   return guarded([&] {
     need(e);
-    DeviceGuard g(e->device);
-    unsigned long long s = 0;
-    ck(cudaMemcpyAsync(&s, e->swaps, sizeof s, cudaMemcpyDeviceToHost, e->stream), "swap read");
-    if (reset) ck(cudaMemsetAsync(e->swaps, 0, sizeof s, e->stream), "swap reset");
-    ck(cudaStreamSynchronize(e->stream), "swap sync");
-    if (swaps) *swaps = s;
+    unsigned long long total = 0;
+    each(e, [&](fhpg_engine* p) {
+      unsigned long long s = 0;
+      ck(cudaMemcpyAsync(&s, p->swaps, sizeof s, cudaMemcpyDeviceToHost, p->stream), "swap read");
+      if (reset) ck(cudaMemsetAsync(p->swaps, 0, sizeof s, p->stream), "swap reset");
+      ck(cudaStreamSynchronize(p->stream), "swap sync");
+      total += s;
+    });
+    if (swaps) *swaps = total;
   });
 }
 
 int fhpg_synchronize(fhpg_engine* e) {
   return guarded([&] {
     need(e);
-    DeviceGuard g(e->device);
-    ck(cudaStreamSynchronize(e->stream), "synchronize");
+    each(e, [&](fhpg_engine* p) { ck(cudaStreamSynchronize(p->stream), "synchronize"); });
   });
 }
 
 int fhpg_reduce_global(fhpg_engine* e, int64_t* mass, int64_t* px, int64_t* py) {
   return guarded([&] {
     need(e);
-    DeviceGuard g(e->device);
-    ck(cudaMemsetAsync(e->acc, 0, sizeof(long long) * 3, e->stream), "acc reset");
-    fhpg::launch_reduce_global(bytes_view(e), e->pitch, e->W, e->nrows, e->acc, e->stream);
-    ck(cudaGetLastError(), "reduce launch");
-    long long h[3];
-    ck(cudaMemcpyAsync(h, e->acc, sizeof h, cudaMemcpyDeviceToHost, e->stream), "acc read");
-    ck(cudaStreamSynchronize(e->stream), "reduce sync");
-    if (mass) *mass = h[0];
-    if (px) *px = h[1];
-    if (py) *py = h[2];
+    long long tot[3] = {0, 0, 0};
+    each(e, [&](fhpg_engine* p) {
+      ck(cudaMemsetAsync(p->acc, 0, sizeof(long long) * 3, p->stream), "acc reset");
+      fhpg::launch_reduce_global(bytes_view(p), p->pitch, p->W, p->nrows, p->acc, p->stream);
+      ck(cudaGetLastError(), "reduce launch");
+      long long h[3];
+      ck(cudaMemcpyAsync(h, p->acc, sizeof h, cudaMemcpyDeviceToHost, p->stream), "acc read");
+      ck(cudaStreamSynchronize(p->stream), "reduce sync");
+      for (int k = 0; k < 3; ++k) tot[k] += h[k];
+    });
+    if (mass) *mass = tot[0];
+    if (px) *px = tot[1];
+    if (py) *py = tot[2];
   });
 }
 
@@ -584,27 +841,45 @@ int fhpg_reduce_cells(fhpg_engine* e, int B, int32_t* nodes, int32_t* particles,
     need(e);
     if (B < 1) invalid("block size must be >= 1");  // observables.cpp:50
     if (!nodes || !particles || !px || !py) invalid("null output array");
-    DeviceGuard g(e->device);
     const size_t cx = (static_cast<size_t>(e->W) + B - 1) / B;
     const size_t cy = (static_cast<size_t>(e->H) - 2 + B - 1) / B;
     const size_t n = cx * cy;
     if (n == 0) return;
-    void* d = nullptr;
-    ck(cudaMallocAsync(&d, n * 24, e->stream), "cudaMallocAsync(cells)");
-    int* dn = static_cast<int*>(d);
-    int* dp = dn + n;
-    long long* dx = reinterpret_cast<long long*>(static_cast<char*>(d) + n * 8);
-    long long* dy = dx + n;
-    ck(cudaMemsetAsync(d, 0, n * 24, e->stream), "cells reset");
-    fhpg::launch_reduce_cells(bytes_view(e), e->pitch, e->W, e->nrows, e->row_begin, e->H, B,
-                              dn, dp, dx, dy, e->stream);
-    ck(cudaGetLastError(), "cells launch");
-    ck(cudaMemcpyAsync(nodes, dn, n * 4, cudaMemcpyDeviceToHost, e->stream), "cells read");
-    ck(cudaMemcpyAsync(particles, dp, n * 4, cudaMemcpyDeviceToHost, e->stream), "cells read");
-    ck(cudaMemcpyAsync(px, dx, n * 8, cudaMemcpyDeviceToHost, e->stream), "cells read");
-    ck(cudaMemcpyAsync(py, dy, n * 8, cudaMemcpyDeviceToHost, e->stream), "cells read");
-    ck(cudaFreeAsync(d, e->stream), "cudaFreeAsync(cells)");
-    ck(cudaStreamSynchronize(e->stream), "cells sync");
+    // One pass per strip into a device grid of the whole lattice's cells
+    // (strips add only their own rows); the host sums the strips.
+    std::vector<int32_t> hn(e->multi() ? n : 0), hp(hn.size());
+    std::vector<int64_t> hx(hn.size()), hy(hn.size());
+    bool first = true;
+    each(e, [&](fhpg_engine* p) {
+      void* d = nullptr;
+      ck(cudaMallocAsync(&d, n * 24, p->stream), "cudaMallocAsync(cells)");
+      int* dn = static_cast<int*>(d);
+      int* dp = dn + n;
+      long long* dx = reinterpret_cast<long long*>(static_cast<char*>(d) + n * 8);
+      long long* dy = dx + n;
+      ck(cudaMemsetAsync(d, 0, n * 24, p->stream), "cells reset");
+      fhpg::launch_reduce_cells(bytes_view(p), p->pitch, p->W, p->nrows, p->row_begin, p->H, B,
+                                dn, dp, dx, dy, p->stream);
+      ck(cudaGetLastError(), "cells launch");
+      int32_t* on = e->multi() ? hn.data() : nodes;
+      int32_t* op = e->multi() ? hp.data() : particles;
+      int64_t* ox = e->multi() ? hx.data() : px;
+      int64_t* oy = e->multi() ? hy.data() : py;
+      ck(cudaMemcpyAsync(on, dn, n * 4, cudaMemcpyDeviceToHost, p->stream), "cells read");
+      ck(cudaMemcpyAsync(op, dp, n * 4, cudaMemcpyDeviceToHost, p->stream), "cells read");
+      ck(cudaMemcpyAsync(ox, dx, n * 8, cudaMemcpyDeviceToHost, p->stream), "cells read");
+      ck(cudaMemcpyAsync(oy, dy, n * 8, cudaMemcpyDeviceToHost, p->stream), "cells read");
+      ck(cudaFreeAsync(d, p->stream), "cudaFreeAsync(cells)");
+      ck(cudaStreamSynchronize(p->stream), "cells sync");
+      if (!e->multi()) return;
+      for (size_t i = 0; i < n; ++i) {
+        nodes[i] = (first ? 0 : nodes[i]) + hn[i];
+        particles[i] = (first ? 0 : particles[i]) + hp[i];
+        px[i] = (first ? 0 : px[i]) + hx[i];
+        py[i] = (first ? 0 : py[i]) + hy[i];
+      }
+      first = false;
+    });
   });
 }
 
@@ -612,21 +887,24 @@ int fhpg_reduce_rows(fhpg_engine* e, int64_t* px, int32_t* fluid) {
   return guarded([&] {
     need(e);
     if (!px || !fluid) invalid("null output array");
-    DeviceGuard g(e->device);
-    const int lo = std::max(1, e->row_begin), hi = std::min(e->H - 1, e->row_end);
-    if (hi <= lo) return;
-    const size_t n = static_cast<size_t>(e->H - 2);
-    void* d = nullptr;
-    ck(cudaMallocAsync(&d, n * 12, e->stream), "cudaMallocAsync(rows)");
-    long long* dx = static_cast<long long*>(d);
-    int* df = reinterpret_cast<int*>(dx + n);
-    fhpg::launch_reduce_rows(bytes_view(e), e->pitch, e->W, e->nrows, e->row_begin, e->H, dx,
-                             df, e->stream);
-    ck(cudaGetLastError(), "rows launch");
-    ck(cudaMemcpyAsync(px + (lo - 1), dx + (lo - 1), (hi - lo) * 8, cudaMemcpyDeviceToHost, e->stream), "rows read");
-    ck(cudaMemcpyAsync(fluid + (lo - 1), df + (lo - 1), (hi - lo) * 4, cudaMemcpyDeviceToHost, e->stream), "rows read");
-    ck(cudaFreeAsync(d, e->stream), "cudaFreeAsync(rows)");
-    ck(cudaStreamSynchronize(e->stream), "rows sync");
+    each(e, [&](fhpg_engine* p) {
+      const int lo = std::max(1, p->row_begin), hi = std::min(p->H - 1, p->row_end);
+      if (hi <= lo) return;
+      const size_t n = static_cast<size_t>(p->H - 2);
+      void* d = nullptr;
+      ck(cudaMallocAsync(&d, n * 12, p->stream), "cudaMallocAsync(rows)");
+      long long* dx = static_cast<long long*>(d);
+      int* df = reinterpret_cast<int*>(dx + n);
+      fhpg::launch_reduce_rows(bytes_view(p), p->pitch, p->W, p->nrows, p->row_begin, p->H, dx,
+                               df, p->stream);
+      ck(cudaGetLastError(), "rows launch");
+      ck(cudaMemcpyAsync(px + (lo - 1), dx + (lo - 1), (hi - lo) * 8, cudaMemcpyDeviceToHost,
+                         p->stream), "rows read");
+      ck(cudaMemcpyAsync(fluid + (lo - 1), df + (lo - 1), (hi - lo) * 4, cudaMemcpyDeviceToHost,
+                         p->stream), "rows read");
+      ck(cudaFreeAsync(d, p->stream), "cudaFreeAsync(rows)");
+      ck(cudaStreamSynchronize(p->stream), "rows sync");
+    });
   });
 }
 
@@ -634,12 +912,13 @@ int fhpg_halo(fhpg_engine* e, void** send_top, void** send_bottom, void** recv_t
               void** recv_bottom, size_t* row_bytes) {
   return guarded([&] {
     need(e);
-    uint8_t* b = e->base(e->cur);
-    if (send_top) *send_top = b;
-    if (send_bottom) *send_bottom = b + static_cast<size_t>(e->nrows - 1) * e->pitch;
-    if (recv_top) *recv_top = b - e->pitch;
-    if (recv_bottom) *recv_bottom = b + static_cast<size_t>(e->nrows) * e->pitch;
-    if (row_bytes) *row_bytes = e->planes ? fhpg::planes_row_bytes(e->W) : static_cast<size_t>(e->W);
+    single_only(e, "fhpg_halo");
+    const Halo h = halo_of(e);
+    if (send_top) *send_top = h.send_top;
+    if (send_bottom) *send_bottom = h.send_bottom;
+    if (recv_top) *recv_top = h.recv_top;
+    if (recv_bottom) *recv_bottom = h.recv_bottom;
+    if (row_bytes) *row_bytes = h.row_bytes;
   });
 }
 
@@ -651,18 +930,39 @@ int fhpg_info(fhpg_engine* e, int* width, int* height, int* row_begin, int* row_
     if (height) *height = e->H;
     if (row_begin) *row_begin = e->row_begin;
     if (row_end) *row_end = e->row_end;
+    const fhpg_engine* p0 = e->multi() ? e->parts[0] : e;
     if (fast_path)
-      *fast_path = e->planes ? 2 : (e->path_pref != 2 && fhpg::fast_path_ok(e->W)) ? 1 : 0;
-    if (step_launches) *step_launches = e->launches;
+      *fast_path = p0->planes ? 2 : (p0->path_pref != 2 && fhpg::fast_path_ok(p0->W)) ? 1 : 0;
+    uint64_t n = 0;
+    if (e->multi())
+      for (const fhpg_engine* p : e->parts) n += p->launches;
+    else
+      n = e->launches;
+    if (step_launches) *step_launches = n;
+  });
+}
+
+int fhpg_strips(fhpg_engine* e, int* n_strips, int* row_begin, int* row_end, int* device) {
+  return guarded([&] {
+    need(e);
+    const int n = e->multi() ? static_cast<int>(e->parts.size()) : 1;
+    if (n_strips) *n_strips = n;
+    for (int i = 0; i < n; ++i) {
+      const fhpg_engine* p = e->multi() ? e->parts[i] : e;
+      if (row_begin) row_begin[i] = p->row_begin;
+      if (row_end) row_end[i] = p->row_end;
+      if (device) device[i] = p->device;
+    }
   });
 }
 
 int fhpg_force_generic(fhpg_engine* e, int on) {
   return guarded([&] {
     need(e);
-    DeviceGuard g(e->device);
-    e->path_pref = on ? 2 : 0;
-    sync_layout(e);
+    each(e, [&](fhpg_engine* p) {
+      p->path_pref = on ? 2 : 0;
+      sync_layout(p);
+    });
   });
 }
 
@@ -670,9 +970,10 @@ int fhpg_select_path(fhpg_engine* e, int path) {
   return guarded([&] {
     need(e);
     if (path < 0 || path > 2) invalid("path must be 0 (auto), 1 (byte fast path) or 2 (generic)");
-    DeviceGuard g(e->device);
-    e->path_pref = path;
-    sync_layout(e);
+    each(e, [&](fhpg_engine* p) {
+      p->path_pref = path;
+      sync_layout(p);
+    });
   });
 }
 

@@ -9,6 +9,9 @@
 // The fast path (W % 16 == 0) lives in fhpg_step_fast.cu; this file holds
 // the generic one-thread-per-site step, init, mask and reduction kernels.
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <type_traits>
 
 #include "fhpg_common.cuh"
@@ -253,6 +256,20 @@ int launch_step(const StepArgs& a0, int num_sms, cudaStream_t st, bool force_gen
     return 1;
   }
   return launch_step_fast(a, num_sms, st);
+}
+
+cudaError_t ensure_smem_optin(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find({kernel, dev});
+  if (it != done.end() && it->second == bytes) return cudaSuccess;
+  err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (err == cudaSuccess) done[{kernel, dev}] = bytes;
+  return err;
 }
 
 void launch_column_keys(uint64_t* zc, uint64_t* zf, uint64_t kc, uint64_t kf, int W,

@@ -47,6 +47,11 @@ struct StepArgs {
                              // 0 = DEFAULT (FHPG_RULES_*)
 };
 
+// Dynamic shared-memory opt-in of `kernel` on the CURRENT device (the
+// attribute is per device: an engine on a second GPU of the same process
+// needs its own). Remembered per (kernel, device, bytes); thread-safe.
+cudaError_t ensure_smem_optin(const void* kernel, int bytes);
+
 // Fast path launcher (fhpg_step_fast.cu).
 int launch_step_fast(const StepArgs& a, int num_sms, cudaStream_t st);
 

@@ -573,12 +573,8 @@ __global__ void __launch_bounds__(kThreads, 1) step_fast_kernel(StepArgs a) {
 
 int launch_step_fast(const StepArgs& a0, int num_sms, cudaStream_t st) {
   StepArgs a = a0;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(step_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    cudaFuncSetAttribute(step_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    attr_set = true;
-  }
+  ensure_smem_optin(reinterpret_cast<const void*>(step_fast_kernel<true>), kSmem);
+  ensure_smem_optin(reinterpret_cast<const void*>(step_fast_kernel<false>), kSmem);
   const int rows = a.row_hi - a.row_lo;
   a.k1 = 1u;
   a.k2 = 2u;

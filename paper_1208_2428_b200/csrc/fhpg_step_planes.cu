@@ -992,12 +992,7 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
       grid = a.nbands * a.segs1 + a.nbands / 2;
     }
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(step_ring_kernel<NW, FORCE, RULE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         RG::kSmem);
-    attr = true;
-  }
+  ensure_smem_optin(reinterpret_cast<const void*>(step_ring_kernel<NW, FORCE, RULE>), RG::kSmem);
 #if FHPG_PDL
   // Programmatic dependent launch: the next step's grid is launched while
   // this one runs and its CTAs take SMs as they free up (griddepcontrol.wait
@@ -1051,12 +1046,7 @@ void launch_nw(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st
   const int smem = smem_bytes<NW, FORCE>(bpc);
   // (The kernel also holds 1 KB of static shared memory for the bulk-copy
   // machinery, so the dynamic opt-in is set to exactly what is used.)
-  static int attr = -1;
-  if (attr != smem) {
-    cudaFuncSetAttribute(step_planes_kernel<NW, FORCE, RULE>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = smem;
-  }
+  ensure_smem_optin(reinterpret_cast<const void*>(step_planes_kernel<NW, FORCE, RULE>), smem);
 #if FHPG_PDL
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);

@@ -39,6 +39,10 @@ SIGNATURES = {
     "fhpg_create": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "fhpg_create_strip": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                     C.POINTER(C.c_void_p)]),
+    "fhpg_create_multi": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                    C.POINTER(C.c_void_p)]),
+    "fhpg_strips": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                              C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "fhpg_destroy": (None, [C.c_void_p]),
     "fhpg_last_error": (C.c_char_p, []),
     "fhpg_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
@@ -144,10 +148,23 @@ class Engine:
     """Device-resident FHP lattice (whole lattice, or one row strip)."""
 
     def __init__(self, width: int, height: int, row_begin: int | None = None,
-                 row_end: int | None = None, device: int | None = None):
+                 row_end: int | None = None, device: int | None = None,
+                 strips: int | None = None, devices=None):
+        """Whole lattice on the current device; a row strip [row_begin,
+        row_end) on `device` (fhpg_create_strip); or, with `strips` (and
+        optionally `devices`, one per strip), the whole lattice split into
+        row strips over several GPUs with the halo exchange done by the
+        library (fhpg_create_multi)."""
         self.lib = load_library()
         h = C.c_void_p()
-        if row_begin is None and row_end is None and device is None:
+        if strips is not None:
+            devs = None
+            if devices is not None:
+                devs = (C.c_int * strips)(*[int(d) for d in devices])
+                if len(devices) != strips:
+                    raise ValueError("one device per strip")
+            _check(self.lib.fhpg_create_multi(width, height, strips, devs, C.byref(h)))
+        elif row_begin is None and row_end is None and device is None:
             _check(self.lib.fhpg_create(width, height, C.byref(h)))
         else:
             rb = 0 if row_begin is None else row_begin
@@ -159,6 +176,15 @@ class Engine:
         w, hh, rb, re, fast, n = self._info()
         self.row_begin, self.row_end = rb, re
         self.nrows = re - rb
+
+    @property
+    def strips(self):
+        """[(row_begin, row_end, device)] of the engine's strips."""
+        n = C.c_int()
+        _check(self.lib.fhpg_strips(self.h, C.byref(n), None, None, None))
+        rb, re, dv = ((C.c_int * n.value)() for _ in range(3))
+        _check(self.lib.fhpg_strips(self.h, C.byref(n), rb, re, dv))
+        return [(rb[i], re[i], dv[i]) for i in range(n.value)]
 
     def _info(self):
         w, h, rb, re, fast = (C.c_int() for _ in range(5))

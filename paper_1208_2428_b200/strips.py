@@ -116,14 +116,14 @@ class LocalStrips:
         halos = [engine_halo_tensors(e, dev) for e, dev in zip(self.engines, self.devices)]
         for i in range(len(self.engines) - 1):
             up, dn = halos[i], halos[i + 1]
-            # strip i's last row -> halo above strip i+1, and back.
-            with torch.cuda.stream(self.streams[self.devices[i + 1]]):
-                dn[2].copy_(up[1], non_blocking=True)
-            with torch.cuda.stream(self.streams[self.devices[i]]):
-                up[3].copy_(dn[0], non_blocking=True)
-        if len(self.streams) > 1:  # cross-device copies: fence all streams
-            for s in self.streams.values():
-                s.synchronize()
+            # A cross-device copy_ runs on the SOURCE device's current stream
+            # and fences the destination's current stream: make both engines'
+            # streams current so the copies are ordered after the previous
+            # step's boundary rows on both sides and before the next launch.
+            with torch.cuda.stream(self.streams[self.devices[i]]), \
+                    torch.cuda.stream(self.streams[self.devices[i + 1]]):
+                dn[2].copy_(up[1], non_blocking=True)  # strip i's last row -> halo above i+1
+                up[3].copy_(dn[0], non_blocking=True)  # strip i+1's first row -> halo below i
 
     def advance(self, seed: int, force_p: float, first_step: int, step_count: int) -> int:
         from .engine import bernoulli_threshold
@@ -145,22 +145,58 @@ class LocalStrips:
 class DistStrips:
     """One strip per rank; `engine` is this rank's strip engine (or any
     object with the same halo_tensors()/advance_async()/swaps() methods,
-    which the CPU gloo tests use)."""
+    which the CPU gloo tests use).
 
-    def __init__(self, engine, rank: int, world: int, halo_tensors=None, group=None):
+    staging="device": the halo rows go straight between the GPUs (NCCL over
+    NVLink); the engine is put on torch's current stream, the stream NCCL
+    orders its transfers against (ncclSend waits for the rows written by the
+    previous step's part 1, req.wait() orders part 1 after the arrival).
+    staging="host": the rows are copied through pinned host buffers and
+    exchanged with a CPU backend (gloo) — the multi-process path for ranks
+    that share one GPU or have no peer path.
+    """
+
+    def __init__(self, engine, rank: int, world: int, halo_tensors=None, group=None,
+                 staging: str = "device"):
         self.engine, self.rank, self.world, self.group = engine, rank, world, group
         self._halo = halo_tensors
+        if staging not in ("device", "host"):
+            raise ValueError("staging must be 'device' or 'host'")
+        self.staging = staging
+        self._host = None
+        if halo_tensors is None and hasattr(engine, "set_stream"):
+            engine.set_stream(torch.cuda.current_stream().cuda_stream)
 
     def _halos(self):
         if self._halo is not None:
             return self._halo()
         return engine_halo_tensors(self.engine, torch.cuda.current_device())
 
+    def _host_exchange(self, st, sb, rt, rb):
+        """Host-staged exchange: D2H of the boundary rows (ordered on the
+        engine stream), CPU-backend P2P, H2D into the halo rows."""
+        n = st.numel()
+        if self._host is None or self._host[0].numel() != n:
+            self._host = [torch.empty(n, dtype=torch.uint8, pin_memory=True) for _ in range(4)]
+        hst, hsb, hrt, hrb = self._host
+        hst.copy_(st)
+        hsb.copy_(sb)  # blocking copies: the rows of the previous step are final
+        exchange_halos(hst, hsb, hrt, hrb, self.rank, self.world, self.group, wait=True)
+        if self.rank > 0:
+            rt.copy_(hrt)
+        if self.rank < self.world - 1:
+            rb.copy_(hrb)
+
     def advance_async(self, seed: int, force_thr: int, first_step: int, step_count: int):
         if self.world == 1:  # no exchange: one call, the step kernels chain the column keys
             self.engine.advance_async(seed, force_thr, first_step, step_count)
             return
         for s in range(first_step, first_step + step_count):
+            if self.staging == "host":
+                self._host_exchange(*self._halos())
+                self.engine.advance_part(seed, force_thr, s, 0)
+                self.engine.advance_part(seed, force_thr, s, 1)
+                continue
             # The exchange of this step's boundary rows is issued first (NCCL
             # waits for the previous step), the interior rows run while it is
             # in flight, the boundary rows after it lands.
