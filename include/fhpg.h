@@ -149,6 +149,18 @@ int fhpg_reduce_global(fhpg_engine* e, int64_t* mass, int64_t* px, int64_t* py);
 int fhpg_reduce_cells(fhpg_engine* e, int block, int32_t* nodes, int32_t* particles,
                       int64_t* px, int64_t* py);
 
+/* The same sums without blocking (the dump pipeline, step.cpp:150-166 /
+ * fhp_main.cpp:52-59, at a dump_every cadence): the reduction and the copy
+ * of its result into engine-owned pinned host memory are enqueued on the
+ * engine's stream(s) behind the steps already enqueued, and the call returns
+ * at once, so the next steps can be enqueued while the sums travel.
+ * fhpg_cells_wait() blocks until they have landed and copies them out
+ * (summed over the strips of a multi-strip engine). One request is
+ * outstanding per engine; a new request first waits for the previous one. */
+int fhpg_reduce_cells_async(fhpg_engine* e, int block);
+int fhpg_cells_wait(fhpg_engine* e, int32_t* nodes, int32_t* particles, int64_t* px,
+                    int64_t* py);
+
 /* velocity_profile integer sums (observables.cpp:84-102): for global interior
  * row r (1..H-2) entry r-1 = (sum px over fluid nodes, fluid node count);
  * only the engine's own rows are written. */

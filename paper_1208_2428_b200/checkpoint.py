@@ -79,7 +79,7 @@ def capture(engine, next_step: int, seed: int, force_p: float, swaps: int, table
 
 def restore(engine, ck: Checkpoint) -> None:
     """Table, obstacles (bit 7) and state back into an engine of the same size."""
-    if getattr(engine, "nrows", None) is not None and (engine.nrows, engine.W) != (ck.H, ck.W):
+    if getattr(engine, "nrows", None) is not None and (engine.nrows, engine.W) != (ck.height, ck.width):
         raise ValueError("checkpoint: engine size differs from the checkpoint's lattice")
     engine.set_table(ck.table)
     engine.set_obstacles((ck.state >> 7).astype(np.uint8))

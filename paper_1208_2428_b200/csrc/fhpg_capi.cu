@@ -39,6 +39,14 @@ struct fhpg_engine {
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   cudaEvent_t tail = nullptr;            // recorded after the last enqueued work (any stream)
+  // Coarse-grain request (fhpg_reduce_cells_async): device sums copied into
+  // pinned host memory on the stream, `cells_ev` marks their arrival.
+  void* cells_dev = nullptr;
+  void* cells_host = nullptr;
+  size_t cells_cap = 0;                  // bytes of each buffer
+  size_t cells_n = 0;                    // cells of the pending request
+  bool cells_pending = false;
+  cudaEvent_t cells_ev = nullptr;
   bool table_set = false;
   bool normalized = true;                // state bit 7 == mask
   int num_sms = 148;
@@ -137,6 +145,9 @@ void release(fhpg_engine* e) {
   cudaFree(e->zkeys);
   cudaFree(e->swaps);
   cudaFree(e->acc);
+  cudaFree(e->cells_dev);
+  cudaFreeHost(e->cells_host);
+  if (e->cells_ev) cudaEventDestroy(e->cells_ev);
   if (e->own_stream) cudaStreamDestroy(e->own_stream);
   if (e->tail) cudaEventDestroy(e->tail);
   delete e;
@@ -182,6 +193,7 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
     ck(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     e->stream = e->own_stream;
     ck(cudaEventCreateWithFlags(&e->tail, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&e->cells_ev, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device),
        "cudaDeviceGetAttribute");
     ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
@@ -822,7 +834,11 @@ int fhpg_reduce_global(fhpg_engine* e, int64_t* mass, int64_t* px, int64_t* py) 
     long long tot[3] = {0, 0, 0};
     each(e, [&](fhpg_engine* p) {
       ck(cudaMemsetAsync(p->acc, 0, sizeof(long long) * 3, p->stream), "acc reset");
-      fhpg::launch_reduce_global(bytes_view(p), p->pitch, p->W, p->nrows, p->acc, p->stream);
+      if (p->planes)
+        fhpg::launch_reduce_global_planes(p->base(p->cur), p->pitch, p->W, p->nrows, p->acc,
+                                          p->num_sms, p->stream);
+      else
+        fhpg::launch_reduce_global(bytes_view(p), p->pitch, p->W, p->nrows, p->acc, p->stream);
       ck(cudaGetLastError(), "reduce launch");
       long long h[3];
       ck(cudaMemcpyAsync(h, p->acc, sizeof h, cudaMemcpyDeviceToHost, p->stream), "acc read");
@@ -835,52 +851,99 @@ int fhpg_reduce_global(fhpg_engine* e, int64_t* mass, int64_t* px, int64_t* py) 
   });
 }
 
-int fhpg_reduce_cells(fhpg_engine* e, int B, int32_t* nodes, int32_t* particles, int64_t* px,
-                      int64_t* py) {
+int fhpg_reduce_cells_async(fhpg_engine* e, int B) {
   return guarded([&] {
     need(e);
     if (B < 1) invalid("block size must be >= 1");  // observables.cpp:50
-    if (!nodes || !particles || !px || !py) invalid("null output array");
     const size_t cx = (static_cast<size_t>(e->W) + B - 1) / B;
     const size_t cy = (static_cast<size_t>(e->H) - 2 + B - 1) / B;
     const size_t n = cx * cy;
-    if (n == 0) return;
-    // One pass per strip into a device grid of the whole lattice's cells
-    // (strips add only their own rows); the host sums the strips.
-    std::vector<int32_t> hn(e->multi() ? n : 0), hp(hn.size());
-    std::vector<int64_t> hx(hn.size()), hy(hn.size());
+    each(e, [&](fhpg_engine* p) {
+      // The previous request's host buffer may still be in use.
+      if (p->cells_pending) ck(cudaEventSynchronize(p->cells_ev), "cells wait");
+      p->cells_pending = false;
+      p->cells_n = n;
+      if (n == 0) return;
+      if (p->cells_cap < n * 24) {
+        cudaFree(p->cells_dev);
+        cudaFreeHost(p->cells_host);
+        p->cells_dev = p->cells_host = nullptr;
+        p->cells_cap = 0;
+        ck(cudaMalloc(&p->cells_dev, n * 24), "cudaMalloc(cells)");
+        ck(cudaMallocHost(&p->cells_host, n * 24), "cudaMallocHost(cells)");
+        p->cells_cap = n * 24;
+      }
+      // [nodes i32 | particles i32 | px i64 | py i64]
+      int* dn = static_cast<int*>(p->cells_dev);
+      int* dp = dn + n;
+      long long* dx = reinterpret_cast<long long*>(static_cast<char*>(p->cells_dev) + n * 8);
+      long long* dy = dx + n;
+      ck(cudaMemsetAsync(p->cells_dev, 0, n * 24, p->stream), "cells reset");
+      if (p->planes)
+        fhpg::launch_reduce_cells_planes(p->base(p->cur), p->pitch, p->W, p->nrows, p->row_begin,
+                                         p->H, B, dn, dp, dx, dy, p->num_sms, p->stream);
+      else
+        fhpg::launch_reduce_cells(bytes_view(p), p->pitch, p->W, p->nrows, p->row_begin, p->H, B,
+                                  dn, dp, dx, dy, p->stream);
+      ck(cudaGetLastError(), "cells launch");
+      ck(cudaMemcpyAsync(p->cells_host, p->cells_dev, n * 24, cudaMemcpyDeviceToHost, p->stream),
+         "cells read");
+      ck(cudaEventRecord(p->cells_ev, p->stream), "cudaEventRecord");
+      p->cells_pending = true;
+    });
+    e->cells_n = n;
+    e->cells_pending = true;
+  });
+}
+
+int fhpg_cells_wait(fhpg_engine* e, int32_t* nodes, int32_t* particles, int64_t* px,
+                    int64_t* py) {
+  return guarded([&] {
+    need(e);
+    if (!e->cells_pending) invalid("no coarse-grain request pending (fhpg_reduce_cells_async)");
+    if (!nodes || !particles || !px || !py) invalid("null output array");
+    const size_t n = e->cells_n;
     bool first = true;
     each(e, [&](fhpg_engine* p) {
-      void* d = nullptr;
-      ck(cudaMallocAsync(&d, n * 24, p->stream), "cudaMallocAsync(cells)");
-      int* dn = static_cast<int*>(d);
-      int* dp = dn + n;
-      long long* dx = reinterpret_cast<long long*>(static_cast<char*>(d) + n * 8);
-      long long* dy = dx + n;
-      ck(cudaMemsetAsync(d, 0, n * 24, p->stream), "cells reset");
-      fhpg::launch_reduce_cells(bytes_view(p), p->pitch, p->W, p->nrows, p->row_begin, p->H, B,
-                                dn, dp, dx, dy, p->stream);
-      ck(cudaGetLastError(), "cells launch");
-      int32_t* on = e->multi() ? hn.data() : nodes;
-      int32_t* op = e->multi() ? hp.data() : particles;
-      int64_t* ox = e->multi() ? hx.data() : px;
-      int64_t* oy = e->multi() ? hy.data() : py;
-      ck(cudaMemcpyAsync(on, dn, n * 4, cudaMemcpyDeviceToHost, p->stream), "cells read");
-      ck(cudaMemcpyAsync(op, dp, n * 4, cudaMemcpyDeviceToHost, p->stream), "cells read");
-      ck(cudaMemcpyAsync(ox, dx, n * 8, cudaMemcpyDeviceToHost, p->stream), "cells read");
-      ck(cudaMemcpyAsync(oy, dy, n * 8, cudaMemcpyDeviceToHost, p->stream), "cells read");
-      ck(cudaFreeAsync(d, p->stream), "cudaFreeAsync(cells)");
-      ck(cudaStreamSynchronize(p->stream), "cells sync");
-      if (!e->multi()) return;
-      for (size_t i = 0; i < n; ++i) {
-        nodes[i] = (first ? 0 : nodes[i]) + hn[i];
-        particles[i] = (first ? 0 : particles[i]) + hp[i];
-        px[i] = (first ? 0 : px[i]) + hx[i];
-        py[i] = (first ? 0 : py[i]) + hy[i];
+      if (!p->cells_pending || n == 0) return;
+      ck(cudaEventSynchronize(p->cells_ev), "cells wait");
+      p->cells_pending = false;
+      const int32_t* hn = static_cast<const int32_t*>(p->cells_host);
+      const int32_t* hp = hn + n;
+      const int64_t* hx = reinterpret_cast<const int64_t*>(static_cast<char*>(p->cells_host) + n * 8);
+      const int64_t* hy = hx + n;
+      if (first) {
+        std::memcpy(nodes, hn, n * 4);
+        std::memcpy(particles, hp, n * 4);
+        std::memcpy(px, hx, n * 8);
+        std::memcpy(py, hy, n * 8);
+      } else {
+        for (size_t i = 0; i < n; ++i) {
+          nodes[i] += hn[i];
+          particles[i] += hp[i];
+          px[i] += hx[i];
+          py[i] += hy[i];
+        }
       }
       first = false;
     });
+    e->cells_pending = false;
   });
+}
+
+int fhpg_reduce_cells(fhpg_engine* e, int B, int32_t* nodes, int32_t* particles, int64_t* px,
+                      int64_t* py) {
+  if (e && (!nodes || !particles || !px || !py)) {
+    g_last_error = "null output array";
+    return FHPG_EINVAL;
+  }
+  const int rc = fhpg_reduce_cells_async(e, B);
+  if (rc != FHPG_OK) return rc;
+  if (e->cells_n == 0) {
+    e->cells_pending = false;
+    return FHPG_OK;
+  }
+  return fhpg_cells_wait(e, nodes, particles, px, py);
 }
 
 int fhpg_reduce_rows(fhpg_engine* e, int64_t* px, int32_t* fluid) {
@@ -895,8 +958,12 @@ int fhpg_reduce_rows(fhpg_engine* e, int64_t* px, int32_t* fluid) {
       ck(cudaMallocAsync(&d, n * 12, p->stream), "cudaMallocAsync(rows)");
       long long* dx = static_cast<long long*>(d);
       int* df = reinterpret_cast<int*>(dx + n);
-      fhpg::launch_reduce_rows(bytes_view(p), p->pitch, p->W, p->nrows, p->row_begin, p->H, dx,
-                               df, p->stream);
+      if (p->planes)
+        fhpg::launch_reduce_rows_planes(p->base(p->cur), p->pitch, p->W, p->nrows, p->row_begin,
+                                        p->H, dx, df, p->stream);
+      else
+        fhpg::launch_reduce_rows(bytes_view(p), p->pitch, p->W, p->nrows, p->row_begin, p->H, dx,
+                                 df, p->stream);
       ck(cudaGetLastError(), "rows launch");
       ck(cudaMemcpyAsync(px + (lo - 1), dx + (lo - 1), (hi - lo) * 8, cudaMemcpyDeviceToHost,
                          p->stream), "rows read");

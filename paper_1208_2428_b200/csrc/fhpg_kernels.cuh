@@ -112,4 +112,14 @@ void launch_reduce_cells(const uint8_t* base, size_t pitch, int W, int nrows, lo
 void launch_reduce_rows(const uint8_t* base, size_t pitch, int W, int nrows, long long row0,
                         long long H, long long* px, int* fluid, cudaStream_t st);
 
+// The same observables on a bit-plane lattice (fhpg_reduce_planes.cu), read
+// straight from the planes of the current buffer (`base` = local row 0).
+void launch_reduce_global_planes(const uint8_t* base, size_t pitch, int W, int nrows,
+                                 long long* acc, int num_sms, cudaStream_t st);
+void launch_reduce_cells_planes(const uint8_t* base, size_t pitch, int W, int nrows,
+                                long long row0, long long H, int B, int* nodes, int* particles,
+                                long long* px, long long* py, int num_sms, cudaStream_t st);
+void launch_reduce_rows_planes(const uint8_t* base, size_t pitch, int W, int nrows, long long row0,
+                               long long H, long long* px, int* fluid, cudaStream_t st);
+
 }  // namespace fhpg

@@ -713,6 +713,16 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 #ifndef FHPG_RING_CONS
 #define FHPG_RING_CONS 31
 #endif
+// Consumers take destination rows from a shared counter (1) instead of the
+// static round-robin (0): a consumer the warp schedulers serve less often
+// does fewer rows instead of holding back the ring.
+#ifndef FHPG_DYN_ROWS
+#define FHPG_DYN_ROWS 1
+#endif
+// Back-off (ns) of the producer between polls of a ring slot's empty barrier.
+#ifndef FHPG_PROD_SLEEP
+#define FHPG_PROD_SLEEP 0
+#endif
 template <int NW, bool FORCE>
 struct RingGeo {
   using G = Geo<NW, FORCE>;
@@ -731,7 +741,8 @@ struct RingGeo {
   static constexpr int kStageOff = kRingOff + kRing * G::kSlot;
   static constexpr int kBarOff = kStageOff + kCons * G::kStageAll;
   static constexpr int kTagOff = kBarOff + 2 * 8 * kRing;
-  static constexpr int kSmem = kTagOff + 4 * kRing;
+  static constexpr int kCtrOff = kTagOff + 4 * kRing;  // dynamic row counters (2 parts)
+  static constexpr int kSmem = kCtrOff + 8;
   static_assert(kSmem <= 232448, "shared memory per CTA");
   static constexpr int kBox = FHPG_BOX_ROWS;     // source rows per TMA box (a "group")
   static constexpr int kGroups = kRing / kBox;   // ring slots of whole groups
@@ -801,6 +812,8 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
       mbar_init(empty + k * 8, 3 * RG::kBox);
       sts32(tags + k * 4, 0xFFFFFFFFu);
     }
+    sts32(sbase + RG::kCtrOff, 0u);
+    sts32(sbase + RG::kCtrOff + 4, 0u);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // The band's column keys, made here from the step keys (they depend on
@@ -836,7 +849,20 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
       const uint32_t ngroups = gA + (nB > 0 ? (static_cast<uint32_t>(nB) + 2 + B - 1) / B : 0u);
       for (uint32_t P = 0; P < ngroups; ++P) {
         const uint32_t k = P % kG;
-        if (P >= kG) mbar_wait(empty + k * 8, (P / kG - 1) & 1u);
+        if (P >= kG) {
+#if FHPG_PROD_SLEEP
+          uint32_t done;
+          for (;;) {
+            asm volatile(
+                "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done) : "r"(empty + k * 8), "r"((P / kG - 1) & 1u) : "memory");
+            if (done) break;
+            __nanosleep(FHPG_PROD_SLEEP);
+          }
+#else
+          mbar_wait(empty + k * 8, (P / kG - 1) & 1u);
+#endif
+        }
         {  // tag: an atomic store (consumers poll it; not a data race)
           uint32_t prev;
           asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(prev) : "r"(tags + k * 4), "r"(P) : "memory");
@@ -892,8 +918,17 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   // Destination rows [Rb, Re) of the current band, warp-interleaved; source
   // row r - 1 sits at ring index ibase + r - Rb. Inlined once per part (one
   // copy inside a loop over the parts measured 8% slower: spills).
-  auto rows = [&](const int Rb, const int Re, const uint32_t ibase) {
+  auto rows = [&](const int Rb, const int Re, const uint32_t ibase, const uint32_t ctr) {
+#if FHPG_DYN_ROWS
+    for (;;) {
+      int r = 0;
+      if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(ctr) : "memory");
+      r = Rb + __shfl_sync(kFull, r, 0);
+      if (r >= Re) break;
+#else
+    (void)ctr;
     for (int r = Rb + warp; r < Re; r += RG::kCons) {
+#endif
       const uint32_t i = ibase + static_cast<uint32_t>(r - Rb);  // ring index of source row r - 1
       const bool first_row = r == Rb, last_row = r == Re - 1;
       constexpr uint32_t kG = RG::kGroups;
@@ -939,7 +974,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
                                L.pad, L.padx, L.pad_band, swaps, release);
       }
   };
-  rows(RA0, RA0 + nA, 0u);
+  rows(RA0, RA0 + nA, 0u, sbase + RG::kCtrOff);
   if (nB > 0) {
     // Extra CTA: on to band bA + 1 once every consumer is done with band bA
     // (the key table is rewritten); the producer streams on meanwhile.
@@ -947,7 +982,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
     make_keys(bA + 1, threadIdx.x, RG::kCons * 32);
     asm volatile("bar.sync 1, %0;" ::"r"(RG::kCons * 32) : "memory");
     set_band(bA + 1);
-    rows(row_lo, row_lo + nB, offB);
+    rows(row_lo, row_lo + nB, offB, sbase + RG::kCtrOff + 4);
   }
   if (lane == 0) bulk_wait_all();  // the stores have landed before the kernel ends
   if (FORCE) {

@@ -61,6 +61,8 @@ SIGNATURES = {
     "fhpg_reduce_global": (C.c_int, [C.c_void_p, i64p, i64p, i64p]),
     "fhpg_reduce_cells": (C.c_int, [C.c_void_p, C.c_int, i32p, i32p, i64p, i64p]),
     "fhpg_reduce_rows": (C.c_int, [C.c_void_p, i64p, i32p]),
+    "fhpg_reduce_cells_async": (C.c_int, [C.c_void_p, C.c_int]),
+    "fhpg_cells_wait": (C.c_int, [C.c_void_p, i32p, i32p, i64p, i64p]),
     "fhpg_halo": (C.c_int, [C.c_void_p, vpp, vpp, vpp, vpp, C.POINTER(C.c_size_t)]),
     "fhpg_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                             C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), u64p]),
@@ -306,6 +308,26 @@ class Engine:
         _check(self.lib.fhpg_reduce_cells(self.h, block, nodes.ctypes.data_as(i32p),
                                           parts.ctypes.data_as(i32p), px.ctypes.data_as(i64p),
                                           py.ctypes.data_as(i64p)))
+        shp = (cy, cx)
+        return nodes.reshape(shp), parts.reshape(shp), px.reshape(shp), py.reshape(shp)
+
+    def cells_async(self, block: int):
+        """Enqueue the coarse-grain sums (fhpg_reduce_cells_async); collect
+        them with cells_wait(). Steps enqueued meanwhile overlap the copy."""
+        _check(self.lib.fhpg_reduce_cells_async(self.h, block))
+        self._cells_block = block
+
+    def cells_wait(self):
+        block = self._cells_block
+        cx, cy = (self.W + block - 1) // block, (self.H - 2 + block - 1) // block
+        n = cx * cy
+        nodes = np.zeros(n, np.int32)
+        parts = np.zeros(n, np.int32)
+        px = np.zeros(n, np.int64)
+        py = np.zeros(n, np.int64)
+        _check(self.lib.fhpg_cells_wait(self.h, nodes.ctypes.data_as(i32p),
+                                        parts.ctypes.data_as(i32p), px.ctypes.data_as(i64p),
+                                        py.ctypes.data_as(i64p)))
         shp = (cy, cx)
         return nodes.reshape(shp), parts.reshape(shp), px.reshape(shp), py.reshape(shp)
 

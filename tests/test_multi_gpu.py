@@ -140,34 +140,41 @@ def test_cfg5_local_strips_digest(n, tables, port):
 
 
 def _cuda_worker(rank, world, port_num, W, H, steps, seed, fp, init, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_num))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import datetime
     import sys
-    sys.path.insert(0, ROOT)
-    import paper_1208_2428_b200 as P
-    from oracle.oracle import Port  # checker only (scrambled input)
-    torch.cuda.set_device(0)
-    rb, re = strip_rows(H, world)[rank]
-    eng = P.Engine(W, H, rb, re, 0)
-    eng.set_table(P.build_table("fhp3"))
-    if init:
-        eng.init(seed, 0.2)
-    else:
-        state, mask = Port().scramble(W, H, seed)
-        eng.set_obstacles(mask[rb:re])
-        eng.upload(state[rb:re])
-    strips = DistStrips(eng, rank, world, staging="host")
-    swaps = strips.advance(seed, P.bernoulli_threshold(fp), 0, steps)
-    mine = torch.from_numpy(eng.download())
-    sizes = [b - a for a, b in strip_rows(H, world)]
-    if rank == 0:
-        parts = [torch.empty((k, W), dtype=torch.uint8) for k in sizes]
-        dist.gather(mine, parts, dst=0)
-        q.put((torch.cat(parts).numpy(), swaps))
-    else:
-        dist.gather(mine, None, dst=0)
-    eng.close()
-    dist.destroy_process_group()
+    import traceback
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_num))
+        dist.init_process_group("gloo", rank=rank, world_size=world,
+                                timeout=datetime.timedelta(seconds=180))
+        sys.path.insert(0, ROOT)
+        import paper_1208_2428_b200 as P
+        from oracle.oracle import Port  # checker only (scrambled input)
+        torch.cuda.set_device(0)
+        rb, re = strip_rows(H, world)[rank]
+        eng = P.Engine(W, H, rb, re, 0)
+        eng.set_table(P.build_table("fhp3"))
+        if init:
+            eng.init(seed, 0.2)
+        else:
+            state, mask = Port().scramble(W, H, seed)
+            eng.set_obstacles(mask[rb:re])
+            eng.upload(state[rb:re])
+        strips = DistStrips(eng, rank, world, staging="host")
+        swaps = strips.advance(seed, P.bernoulli_threshold(fp), 0, steps)
+        mine = torch.from_numpy(eng.download())
+        sizes = [b - a for a, b in strip_rows(H, world)]
+        if rank == 0:
+            parts = [torch.empty((k, W), dtype=torch.uint8) for k in sizes]
+            dist.gather(mine, parts, dst=0)
+            q.put(("ok", torch.cat(parts).numpy(), swaps))
+        else:
+            dist.gather(mine, None, dst=0)
+        eng.close()
+        dist.destroy_process_group()
+    except BaseException:
+        q.put(("err", f"rank {rank}: " + traceback.format_exc(), None))
+        raise
 
 
 def _free_port():
@@ -184,9 +191,13 @@ def _run_cuda_world(world, W, H, steps, seed, fp, init):
     procs = mp.start_processes(_cuda_worker,
                                args=(world, _free_port(), W, H, steps, seed, fp, init, q),
                                nprocs=world, join=False, start_method="spawn")
-    got = q.get(timeout=600)
-    procs.join()
-    return got
+    status, got, swaps = q.get(timeout=400)
+    for p in procs.processes:
+        p.join(timeout=60 if status == "ok" else 5)
+        if p.is_alive():
+            p.kill()
+    assert status == "ok", got
+    return got, swaps
 
 
 @pytest.mark.gpu
