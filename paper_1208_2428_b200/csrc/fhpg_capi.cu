@@ -30,7 +30,7 @@ struct fhpg_engine {
   int planes_rule = 2;                   // circuit of the table: FHPG_RULES_* (fhpg_tables.h)
   int path_pref = 0;                     // 0 auto, 1 byte fast path, 2 generic
   uint8_t* scratch = nullptr;            // nrows * pitch
-  alignas(64) unsigned char tmap[2][4][128];  // TMA descriptors of buf[0], buf[1] (planes)
+  alignas(64) unsigned char tmap[2][fhpg::kPlaneMaps][128];  // TMA descriptors of buf[0], buf[1] (planes)
   bool scratch_valid = false;
   uint8_t* table = nullptr;              // 512 bytes
   uint64_t* zkeys = nullptr;             // [parity][purpose][W]
@@ -179,7 +179,7 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
     for (int i = 0; i < 2; ++i) {
       ck(cudaMalloc(&e->buf[i], bytes), "cudaMalloc(state)");
       ck(cudaMemset(e->buf[i], 0, bytes), "cudaMemset(state)");
-      for (int kind = 0; kind < 4 && fhpg::planes_ok(W); ++kind)
+      for (int kind = 0; kind < fhpg::kPlaneMaps && fhpg::planes_ok(W); ++kind)
         if (!fhpg::make_planes_map(e->tmap[i][kind], e->buf[i], W, e->pitch, e->nrows + 5, kind))
           throw Failure{FHPG_ERUNTIME, "cuTensorMapEncodeTiled failed"};
     }
@@ -261,9 +261,8 @@ void sync_layout(fhpg_engine* e) {
 void launch_any(fhpg_engine* e, const fhpg::StepArgs& a) {
   if (e->planes) {
     const int which = a.src == e->base(0) ? 0 : 1;
-    e->launches += fhpg::launch_step_planes(a, e->tmap[which][0], e->tmap[which ^ 1][1],
-                                            e->tmap[which ^ 1][2], e->tmap[which][3],
-                                            e->num_sms, e->stream);
+    e->launches += fhpg::launch_step_planes(a, e->tmap[which], e->tmap[which ^ 1], e->num_sms,
+                                            e->stream);
     e->scratch_valid = false;
   } else {
     e->launches += fhpg::launch_step(a, e->num_sms, e->stream, e->path_pref == 2);
@@ -834,7 +833,7 @@ int fhpg_reduce_global(fhpg_engine* e, int64_t* mass, int64_t* px, int64_t* py) 
     long long tot[3] = {0, 0, 0};
     each(e, [&](fhpg_engine* p) {
       ck(cudaMemsetAsync(p->acc, 0, sizeof(long long) * 3, p->stream), "acc reset");
-      if (p->planes)
+      if (p->planes && !p->scratch_valid)  // else: the exact uploaded bytes
         fhpg::launch_reduce_global_planes(p->base(p->cur), p->pitch, p->W, p->nrows, p->acc,
                                           p->num_sms, p->stream);
       else
@@ -879,7 +878,7 @@ int fhpg_reduce_cells_async(fhpg_engine* e, int B) {
       long long* dx = reinterpret_cast<long long*>(static_cast<char*>(p->cells_dev) + n * 8);
       long long* dy = dx + n;
       ck(cudaMemsetAsync(p->cells_dev, 0, n * 24, p->stream), "cells reset");
-      if (p->planes)
+      if (p->planes && !p->scratch_valid)  // else: the exact uploaded bytes
         fhpg::launch_reduce_cells_planes(p->base(p->cur), p->pitch, p->W, p->nrows, p->row_begin,
                                          p->H, B, dn, dp, dx, dy, p->num_sms, p->stream);
       else
@@ -958,7 +957,7 @@ int fhpg_reduce_rows(fhpg_engine* e, int64_t* px, int32_t* fluid) {
       ck(cudaMallocAsync(&d, n * 12, p->stream), "cudaMallocAsync(rows)");
       long long* dx = static_cast<long long*>(d);
       int* df = reinterpret_cast<int*>(dx + n);
-      if (p->planes)
+      if (p->planes && !p->scratch_valid)  // else: the exact uploaded bytes
         fhpg::launch_reduce_rows_planes(p->base(p->cur), p->pitch, p->W, p->nrows, p->row_begin,
                                         p->H, dx, df, p->stream);
       else

@@ -64,17 +64,19 @@ bool fast_path_ok(int W);
 bool planes_ok(int W);  // W % 1024 == 0
 int planes_words_per_lane(int W);
 size_t planes_row_bytes(int W);
-// TMA descriptor (CUtensorMap, 64-byte aligned, 128 bytes) of a plane buffer
-// whose row 0 is at `buffer` (the top halo row), `rows` rows; kind 0 = row
-// loads (band + edge words, 8 planes), 1 = band stores (7 planes), 2 = pad
-// stores (4 words, 7 planes), 3 = two-row loads.
+// TMA descriptors (CUtensorMap, 64-byte aligned, 128 bytes each) of a plane
+// buffer whose row 0 is at `buffer` (the top halo row), `rows` rows: kind 0
+// = row loads (band + edge words, 8 planes), 1 = band stores (7 planes), 2 =
+// pad stores (4 words, 7 planes), 3 = FHPG_BOX_ROWS-row loads, 4 / 5 = 2-row
+// band / pad stores.
+constexpr int kPlaneMaps = 6;
 bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows, int kind);
-// One time step with a collision circuit (a.rule) over rows [row_lo, row_hi): loads
-// through the source buffer's kind-0 map, stores through the destination
-// buffer's kind-1 / kind-2 maps.
-int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap_dst_store,
-                       const void* tmap_dst_pad, const void* tmap_src_pair, int num_sms,
-                       cudaStream_t st);
+// One time step with a collision circuit (a.rule) over rows [row_lo, row_hi)
+// (and the optional second range): loads through the source buffer's maps,
+// stores through the destination buffer's (src_maps / dst_maps: the
+// kPlaneMaps descriptors of each buffer, in kind order).
+int launch_step_planes(const StepArgs& a, const void* src_maps, const void* dst_maps,
+                       int num_sms, cudaStream_t st);
 // Bytes (rows 0..nrows-1 of src) -> planes in dst; plane 7 from the mask,
 // also written into dst_obst (the other ping-pong buffer).
 void launch_pack_planes(const uint8_t* src, const uint8_t* mask, uint8_t* dst, uint8_t* dst_obst,

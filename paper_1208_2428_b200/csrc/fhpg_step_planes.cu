@@ -714,12 +714,12 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 #define FHPG_RING_CONS 31
 #endif
 // Consumers take destination rows from a shared counter (1) instead of the
-// static round-robin (0): a consumer the warp schedulers serve less often
-// does fewer rows instead of holding back the ring.
+// static round-robin (0) (measured: 2097 vs 2111 GSUPS on cfg4, kept off).
 #ifndef FHPG_DYN_ROWS
-#define FHPG_DYN_ROWS 1
+#define FHPG_DYN_ROWS 0
 #endif
-// Back-off (ns) of the producer between polls of a ring slot's empty barrier.
+// Back-off (ns) of the producer between polls of a ring slot's empty barrier
+// (measured: no effect at 200 or 1000 ns).
 #ifndef FHPG_PROD_SLEEP
 #define FHPG_PROD_SLEEP 0
 #endif
@@ -992,10 +992,523 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   }
 }
 
-template <int NW, bool FORCE, int RULE>
-void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st) {
+// ---------------------------------------------------------------------------
+// Row-pair ring kernel (default for the 2048-column bands). The same shared
+// row ring as step_ring_kernel, but a consumer warp takes two destination
+// rows at a time (rows r, r+1 from source rows r-1 .. r+2): the per-row
+// costs of the ring protocol (slot waits and releases), of the chirality
+// walk's setup (one balanced walk over both rows' sites) and of the output
+// (one TMA store of a 2-row box) are paid once per pair. Registers: up to
+// 128 per thread, 16 consumer warps (+ the producer).
+// ---------------------------------------------------------------------------
+#ifndef FHPG_PAIR_CONS
+#define FHPG_PAIR_CONS 15
+#endif
+#ifndef FHPG_PAIR_RING
+#define FHPG_PAIR_RING 64
+#endif
+#ifndef FHPG_PAIR_RING_F
+#define FHPG_PAIR_RING_F 32
+#endif
+#ifndef FHPG_PAIR
+#define FHPG_PAIR 0
+#endif
+template <int NW, bool FORCE>
+struct PairGeo {
   using G = Geo<NW, FORCE>;
-  using RG = RingGeo<NW, FORCE>;
+  static constexpr int kCons = FHPG_PAIR_CONS;
+  static constexpr int kRing = FORCE ? FHPG_PAIR_RING_F : FHPG_PAIR_RING;
+  static constexpr int kThreads = (kCons + 1) * 32;
+  static constexpr int kKeys = (FORCE ? 2 : 1) * G::kBandCols * 8;
+  static constexpr int kRingOff = (kKeys + 127) / 128 * 128;
+  // Per consumer: the outputs of two rows [row][plane][band words] (the
+  // 2-row TMA store box), then the two 2-row pad boxes [row][plane][4 words].
+  // The walk's list (up to 2 x 32 NW entries) and result words (2 rows) live
+  // in the output area while it is dead.
+  static constexpr int kRowOut = G::kStage;  // 7 planes x band words x 4 B
+  static constexpr int kPadL = 2 * kRowOut, kPadR = 2 * kRowOut + 256;
+  static constexpr int kList = 0;
+  static constexpr int kOut = 16 * 2 * 32 * NW;
+  static constexpr int kStage = 2 * kRowOut + 512;
+  static_assert(kOut + 2 * 4 * 32 * NW <= 2 * kRowOut, "walk scratch must fit the output area");
+  static constexpr int kStageOff = kRingOff + kRing * G::kSlot;
+  static constexpr int kBarOff = kStageOff + kCons * kStage;
+  static constexpr int kTagOff = kBarOff + 2 * 8 * kRing;
+  static constexpr int kCtrOff = kTagOff + 4 * kRing;  // dynamic pair counters (2 parts)
+  static constexpr int kSmem = kCtrOff + 8;
+  static_assert(kSmem <= 232448, "shared memory per CTA");
+  static constexpr int kBox = FHPG_BOX_ROWS;
+  static constexpr int kGroups = kRing / kBox;
+  static_assert(kRing % kBox == 0, "row groups");
+};
+
+// The planes of destination row r (parity Q) pulled from the ring slots of
+// rows r-1 (sm), r (sc), r+1 (sn) (backends.cpp:64-73, as in dest_row).
+template <int NW, int Q>
+__device__ __forceinline__ void pull_row(uint32_t sm, uint32_t sc, uint32_t sn,
+                                         uint32_t (&a)[6][NW], uint32_t (&rr)[NW],
+                                         uint32_t (&so)[NW]) {
+  constexpr int P = Geo<NW, false>::kPlane;
+  if (Q) rd_shr<NW>(sn + 0 * P, a[0]); else rd_al<NW>(sn + 0 * P, a[0]);
+  if (Q) rd_al<NW>(sn + 1 * P, a[1]); else rd_shl<NW>(sn + 1 * P, a[1]);
+  rd_shl<NW>(sc + 2 * P, a[2]);
+  if (Q) rd_al<NW>(sm + 3 * P, a[3]); else rd_shl<NW>(sm + 3 * P, a[3]);
+  if (Q) rd_shr<NW>(sm + 4 * P, a[4]); else rd_al<NW>(sm + 4 * P, a[4]);
+  rd_shr<NW>(sc + 5 * P, a[5]);
+  rd_al<NW>(sc + 6 * P, rr);
+  rd_al<NW>(sc + 7 * P, so);
+}
+
+// The balanced walk of `walk` over the set bits of two rows' masks (m[0]:
+// row r, m[1]: row r + 1). List entries carry the row in bit 31 of the
+// sites-before field; fn(key address, row) returns the site's bit, ORed into
+// the result words [row][band word] at osm.
+template <int NW, int NR, typename Fn>
+__device__ __forceinline__ int walk_rows(const uint32_t (&m)[2][NW], uint32_t lsm, uint32_t osm,
+                                         uint32_t keys, int lane, const Fn& fn) {
+  int cnt = 0, nz = 0;
+#pragma unroll
+  for (int q = 0; q < NR; ++q)
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      cnt += __popc(m[q][w]);
+      nz += m[q][w] != 0u;
+    }
+  const int packed = cnt | (nz << 16);
+  int incl = packed;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const int T = __shfl_sync(kFull, incl, 31) & 0xFFFF;
+  if (T == 0) return 0;
+  const int excl = incl - packed;
+  {
+    int q0 = excl >> 16, c = excl & 0xFFFF;
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t wi = static_cast<uint32_t>(lane * NW + w);
+        const uint32_t ow = osm + (static_cast<uint32_t>(q) * 32u * NW + wi) * 4u;
+        if (m[q][w]) {
+          sts128(lsm + q0 * 16, m[q][w], keys + wi * 256u,
+                 static_cast<uint32_t>(c) | (static_cast<uint32_t>(q) << 31), ow);
+          ++q0;
+          c += __popc(m[q][w]);
+        }
+        sts32(ow, 0u);
+      }
+  }
+  __syncwarp();
+  const int s = (lane * T) >> 5;
+  const int e = ((lane + 1) * T) >> 5;
+  const int icnt = incl & 0xFFFF;
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step; step >>= 1) {
+    const int v = __shfl_sync(kFull, icnt, o + step - 1);
+    if (v <= s) o += step;
+  }
+  const int o_excl = __shfl_sync(kFull, excl, o);
+  if (s < e) {
+    uint32_t qa = lsm + (o_excl >> 16) * 16u;
+    uint4 en = lds128(qa);
+#pragma unroll
+    for (int w = 1; w < NR * NW; ++w) {
+      if (s >= static_cast<int>(en.z & 0x7FFFFFFFu) + __popc(en.x)) {
+        qa += 16u;
+        en = lds128(qa);
+      }
+    }
+    uint32_t mask = en.x, kw = en.y, ow = en.w, dy = en.z >> 31;
+    for (int k = s - static_cast<int>(en.z & 0x7FFFFFFFu); k > 0; --k) mask &= mask - 1u;
+    auto next = [&](uint32_t& ka, uint32_t& wa, uint32_t& v, uint32_t& row) {
+      if (mask == 0u) {
+        qa += 16u;
+        const uint4 n = lds128(qa);
+        mask = n.x;
+        kw = n.y;
+        ow = n.w;
+        dy = n.z >> 31;
+      }
+      v = mask & (0u - mask);
+      mask ^= v;
+      ka = kw + top_bit(v) * 8u;
+      wa = ow;
+      row = dy;
+    };
+    int it = s;
+    for (; it + 1 < e; it += 2) {
+      uint32_t k0, w0, v0, r0, k1, w1, v1, r1;
+      next(k0, w0, v0, r0);
+      next(k1, w1, v1, r1);
+      const uint32_t b0 = fn(k0, r0), b1 = fn(k1, r1);
+      red_or(w0, b0 * v0);
+      red_or(w1, b1 * v1);
+    }
+    if (it < e) {
+      uint32_t k0, w0, v0, r0;
+      next(k0, w0, v0, r0);
+      red_or(w0, fn(k0, r0) * v0);
+    }
+  }
+  __syncwarp();
+  return T;
+}
+
+// Per-site result bits of the walks (functors with forced inlining: lambdas
+// passed down here were kept out of line, their closures in local memory).
+struct ChirBit {
+  uint32_t y, four;
+  __device__ __forceinline__ uint32_t operator()(uint32_t ka, uint32_t row) const {
+    return chir_bit(lds64(ka) + (y + row), four);
+  }
+};
+struct ForceBit {
+  uint32_t y;
+  uint64_t thr;
+  __device__ __forceinline__ uint32_t operator()(uint32_t ka, uint32_t row) const {
+    return (fin64(lds64(ka) + (y + row)) >> 32) < thr ? 1u : 0u;
+  }
+};
+
+// Empty-barrier arrivals of a pair's source rows r-1 .. r+2 (ring index i
+// of row r-1): one per (destination row, source row) use, plus the missing
+// destination rows outside [Rb, Re) at the part's edges, 3 per source row.
+struct PairRelease {
+  uint32_t empty, i;
+  int lane;
+  bool two, first, last;
+  template <uint32_t B, uint32_t kG>
+  __device__ __forceinline__ void arrive() const {
+    __syncwarp();
+    if (lane == 0) {
+      uint32_t c0 = 1u, c1 = two ? 2u : 1u, c2 = two ? 2u : 1u, c3 = two ? 1u : 0u;
+      if (first) {
+        c0 += 2u;
+        c1 += 1u;
+      }
+      if (last) {  // source rows Re (2 missing users) and Re - 1 (1)
+        if (two) {
+          c3 += 2u;
+          c2 += 1u;
+        } else {
+          c2 += 2u;
+          c1 += 1u;
+        }
+      }
+      const uint32_t g0 = i / B;
+      uint32_t s0 = c0, s1 = 0;
+      ((i + 1) / B == g0 ? s0 : s1) += c1;
+      ((i + 2) / B == g0 ? s0 : s1) += c2;
+      ((i + 3) / B == g0 ? s0 : s1) += c3;
+      mbar_arrive(empty + (g0 % kG) * 8, s0);
+      if (s1) mbar_arrive(empty + ((g0 + 1) % kG) * 8, s1);
+    }
+  }
+};
+
+// Destination rows r (parity Q) and, when NR == 2, r + 1, from the slots of
+// source rows r-1 .. r+NR (sl[0..NR+1], this lane's word address in plane
+// 0). `released()` is called once the source rows are in registers.
+template <int NW, bool FORCE, int RULE, int Q, int NR>
+__device__ __forceinline__ void dest_rows(const uint32_t (&sl)[4], uint32_t stage,
+                                          const Ctx<NW, FORCE>& cx, int lane, uint32_t y,
+                                          const CUtensorMap* stmap, const CUtensorMap* padmap,
+                                          int w0, int trow, int pad, int padx, bool pad_band,
+                                          unsigned& swaps, const PairRelease& rel) {
+  using PG = PairGeo<NW, FORCE>;
+  uint32_t a[2][6][NW], rr[2][NW], so[2][NW];
+  pull_row<NW, Q>(sl[0], sl[1], sl[2], a[0], rr[0], so[0]);
+  if constexpr (NR == 2) pull_row<NW, Q ^ 1>(sl[1], sl[2], sl[3], a[1], rr[1], so[1]);
+  rel.arrive<PG::kBox, PG::kGroups>();
+  typename PlaneRule<RULE>::Class K[2][NW];
+  uint32_t dep[2][NW];
+#pragma unroll
+  for (int q = 0; q < NR; ++q)
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t aw[6] = {a[q][0][w], a[q][1][w], a[q][2][w], a[q][3][w], a[q][4][w], a[q][5][w]};
+      K[q][w] = PlaneRule<RULE>::classify(aw, rr[q][w], so[q][w]);
+      dep[q][w] = K[q][w].dep;
+    }
+  // The previous pair's TMA stores must have read the output area (which
+  // also holds the walk scratch) before it is rewritten.
+  if (lane == 0) bulk_wait_read();
+  __syncwarp();
+  const uint32_t lsm = stage + PG::kList, osm = stage + PG::kOut;
+  // Chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y)
+  // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76).
+  const int T = walk_rows<NW, NR>(dep, lsm, osm, cx.kc, lane, ChirBit{y, cx.four});
+  uint32_t o[2][NW][7];
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    const uint32_t mine = osm + (static_cast<uint32_t>(q) * 32u * NW + lane * NW) * 4u;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const uint32_t c = T ? lds32(mine + w * 4) : 0u;
+      uint32_t oo[6], orr;
+      const uint32_t aw[6] = {a[q][0][w], a[q][1][w], a[q][2][w], a[q][3][w], a[q][4][w], a[q][5][w]};
+      PlaneRule<RULE>::apply(K[q][w], c, rr[q][w], aw, oo, orr, so[q][w]);
+#pragma unroll
+      for (int p = 0; p < 6; ++p) o[q][w][p] = oo[p];
+      o[q][w][6] = orr;
+    }
+  }
+  if constexpr (FORCE) {
+    // step.cpp:79-88: fluid, W (bit 5) set, E (bit 2) clear after collision.
+    uint32_t f[2][NW];
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) f[q][w] = ~so[q][w] & o[q][w][5] & ~o[q][w][2];
+    const int TF = walk_rows<NW, NR>(f, lsm, osm, cx.kf, lane, ForceBit{y, cx.thr});
+    if (TF) {
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const uint32_t mine = osm + (static_cast<uint32_t>(q) * 32u * NW + lane * NW) * 4u;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const uint32_t acc = lds32(mine + w * 4);
+          o[q][w][5] ^= acc;
+          o[q][w][2] ^= acc;
+          swaps += __popc(acc);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NR; ++q)
+#pragma unroll
+    for (int p = 0; p < 7; ++p) {
+      uint32_t v[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) v[w] = o[q][w][p];
+      stsv<NW>(stage + q * PG::kRowOut + p * (4 * 32 * NW) + lane * NW * 4, v);
+      // periodic wrap copies: lanes holding words 0..3 / WW-4..WW-1
+      if (pad_band && pad >= 0) stsv<NW>(stage + pad + q * 112 + p * 16, v);
+    }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store(stmap, w0 + 4, trow, stage);
+    if (pad_band) {
+      if (padx & 1) tma_store(padmap, 0, trow, stage + PG::kPadL);
+      if (padx & 2) tma_store(padmap, (padx >> 2) + 4, trow, stage + PG::kPadR);
+    }
+    bulk_commit();
+  }
+}
+
+template <int NW, bool FORCE, int RULE>
+__global__ void __launch_bounds__(PairGeo<NW, FORCE>::kThreads, 1)
+    step_pair_kernel(StepArgs a, const __grid_constant__ CUtensorMap ldmap,
+                     const __grid_constant__ CUtensorMap stmap1,
+                     const __grid_constant__ CUtensorMap padmap1,
+                     const __grid_constant__ CUtensorMap stmap2,
+                     const __grid_constant__ CUtensorMap padmap2) {
+  using G = Geo<NW, FORCE>;
+  using PG = PairGeo<NW, FORCE>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  // Work split as in step_ring_kernel: part A = band bA, rows [RA0, RA0+nA);
+  // extra CTAs also do part B = band bA + 1 over the same rows.
+  const int nmain = a.nbands * (a.segs1 + a.segs2);
+  int bA, RA0, nA, nB = 0;
+  int row_lo;
+  if (static_cast<int>(blockIdx.x) < nmain) {
+    bA = blockIdx.x % a.nbands;
+    const bool second = static_cast<int>(blockIdx.x / a.nbands) >= a.segs1;
+    const int seg_group = blockIdx.x / a.nbands - (second ? a.segs1 : 0);
+    row_lo = second ? a.row_lo2 : a.row_lo;
+    const int row_hi = second ? a.row_hi2 : a.row_hi - a.extra_rows;
+    RA0 = row_lo + seg_group * a.seg_rows;
+    nA = max(0, min(row_hi, RA0 + a.seg_rows) - RA0);
+  } else {
+    bA = 2 * (blockIdx.x - nmain);
+    row_lo = a.row_hi - a.extra_rows;
+    RA0 = row_lo;
+    nA = a.extra_rows;
+    nB = bA + 1 < a.nbands ? a.extra_rows : 0;
+  }
+  constexpr uint32_t B = PG::kBox;
+  const uint32_t offB = (static_cast<uint32_t>(nA) + 2 + B - 1) / B * B;
+  const uint32_t kc_base = sbase;
+  const uint32_t kf_base = sbase + G::kBandCols * 8;
+  const uint32_t ring = sbase + PG::kRingOff;
+  const uint32_t full = sbase + PG::kBarOff;
+  const uint32_t empty = full + 8 * PG::kRing;
+  const uint32_t tags = sbase + PG::kTagOff;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < PG::kRing; ++k) {
+      mbar_init(full + k * 8, 1);
+      mbar_init(empty + k * 8, 3 * PG::kBox);
+      sts32(tags + k * 4, 0xFFFFFFFFu);
+    }
+    sts32(sbase + PG::kCtrOff, 0u);
+    sts32(sbase + PG::kCtrOff + 4, 0u);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // (The lambdas below capture plain locals, not the kernel parameter `a`:
+  // capturing it by reference puts the whole StepArgs in local memory.)
+  const uint64_t kc_cur = a.kc_cur, kf_cur = a.kf_cur;
+  const int row0 = static_cast<int>(a.row0);  // global rows < 2^31
+  auto make_keys = [&](int b, int t0, int nt) {
+    for (int c = t0; c < G::kBandCols; c += nt) {
+      const uint64_t x = static_cast<uint64_t>(b * G::kBandCols + c) + 1;
+      sts64(kc_base + c * 8, column_key(kc_cur, x));
+      if (FORCE) sts64(kf_base + c * 8, column_key(kf_cur, x));
+    }
+  };
+  make_keys(bA, threadIdx.x, blockDim.x);
+#if FHPG_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+  if (a.zc_next) {
+    const int n = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.W; i += n) {
+      a.zc_next[i] = column_key(a.kc_next, static_cast<uint64_t>(i) + 1);
+      if (a.zf_next) a.zf_next[i] = column_key(a.kf_next, static_cast<uint64_t>(i) + 1);
+    }
+  }
+  __syncthreads();
+  if (nA + nB <= 0) return;
+
+  if (warp == PG::kCons) {  // producer (tensor row = local row + 1)
+    if (lane == 0) {
+      constexpr uint32_t kG = PG::kGroups;
+      const uint32_t gA = offB / B;
+      const uint32_t ngroups = gA + (nB > 0 ? (static_cast<uint32_t>(nB) + 2 + B - 1) / B : 0u);
+      for (uint32_t P = 0; P < ngroups; ++P) {
+        const uint32_t k = P % kG;
+        if (P >= kG) mbar_wait(empty + k * 8, (P / kG - 1) & 1u);
+        {
+          uint32_t prev;
+          asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(prev) : "r"(tags + k * 4), "r"(P) : "memory");
+        }
+        const bool inA = P < gA;
+        const int word = (inA ? bA : bA + 1) * G::kBandWords;
+        const int trow = inA ? RA0 + static_cast<int>(B * P) : row_lo + static_cast<int>(B * P - offB);
+        mbar_expect_tx(full + k * 8, B * G::kRowBytes);
+        tma_row(ring + B * k * G::kSlot, &ldmap, word, trow, full + k * 8);
+        if (nB > 0 && P + 1 == gA && offB > static_cast<uint32_t>(nA) + 2)
+          mbar_arrive(empty + k * 8, 3 * (offB - static_cast<uint32_t>(nA) - 2));
+      }
+    }
+    return;
+  }
+
+  Lanes L;
+  L.lane = lane;
+  L.WW = a.W >> 5;
+  L.PW = L.WW + 8;
+  auto set_band = [&](int b) {
+    L.w0 = b * G::kBandWords;
+    const int wl = L.w0 + L.lane * NW;
+    L.pad = wl < 4 ? PG::kPadR + wl * 4 : (wl >= L.WW - 4 ? PG::kPadL + (wl - (L.WW - 4)) * 4 : -1);
+    L.padx = (L.w0 + G::kBandWords == L.WW ? 1 : 0) | (L.w0 == 0 ? 2 : 0) | (L.WW << 2);
+    L.pad_band = L.w0 == 0 || L.w0 + G::kBandWords == L.WW;
+  };
+  set_band(bA);
+  const uint32_t stage = sbase + PG::kStageOff + warp * PG::kStage;
+  Ctx<NW, FORCE> cx;
+  cx.kc = kc_base;
+  cx.kf = kf_base;
+  cx.lsm = stage + PG::kList;
+  cx.osm = stage + PG::kOut;
+  cx.stage = stage;
+  cx.thr = a.thr;
+  cx.four = a.k4;
+  unsigned swaps = 0;
+  const uint32_t lane_off = 16u + lane * NW * 4u;
+  const uint32_t y0 = static_cast<uint32_t>(a.row0);
+  // Destination rows [Rb, Re) in pairs, pair j to consumer j mod kCons;
+  // source row r - 1 of the pair at r sits at ring index ibase + r - Rb.
+  auto rows = [&](const int Rb, const int Re, const uint32_t ibase, const uint32_t ctr)
+                  __attribute__((always_inline)) {
+#if FHPG_DYN_ROWS
+    for (;;) {
+      int r = 0;
+      if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 2;" : "=r"(r) : "r"(ctr) : "memory");
+      r = Rb + __shfl_sync(kFull, r, 0);
+      if (r >= Re) break;
+#else
+    (void)ctr;
+    for (int r = Rb + 2 * warp; r < Re; r += 2 * PG::kCons) {
+#endif
+      const bool two = r + 1 < Re;
+      const uint32_t i = ibase + static_cast<uint32_t>(r - Rb);
+      constexpr uint32_t kG = PG::kGroups;
+      const uint32_t nsrc = two ? 4u : 3u;
+      uint32_t sl[4];
+#pragma unroll
+      for (uint32_t d = 0; d < 4; ++d) {
+        if (d < nsrc) {
+          const uint32_t P = (i + d) / B;
+          if (d == 0 || ((i + d) % B) == 0) {
+            const uint32_t kp = P % kG;
+            for (;;) {
+              uint32_t tag;
+              asm volatile("ld.relaxed.cta.shared.u32 %0, [%1];" : "=r"(tag) : "r"(tags + kp * 4) : "memory");
+              if (tag == P) break;
+              __nanosleep(FHPG_TAG_SLEEP);
+            }
+            mbar_wait(full + kp * 8, (P / kG) & 1u);
+          }
+          sl[d] = ring + ((i + d) % PG::kRing) * G::kSlot + lane_off;
+        } else {
+          sl[d] = sl[d - 1];
+        }
+      }
+      const PairRelease rel{empty, i, lane, two, r == Rb, r + (two ? 1 : 0) == Re - 1};
+      const bool q = (row0 + r) & 1;
+      if (two) {
+        if (q)
+          dest_rows<NW, FORCE, RULE, 1, 2>(sl, stage, cx, lane, y0 + r, &stmap2, &padmap2, L.w0, r + 1,
+                                           L.pad, L.padx, L.pad_band, swaps, rel);
+        else
+          dest_rows<NW, FORCE, RULE, 0, 2>(sl, stage, cx, lane, y0 + r, &stmap2, &padmap2, L.w0, r + 1,
+                                           L.pad, L.padx, L.pad_band, swaps, rel);
+      } else {
+        if (q)
+          dest_rows<NW, FORCE, RULE, 1, 1>(sl, stage, cx, lane, y0 + r, &stmap1, &padmap1, L.w0, r + 1,
+                                           L.pad, L.padx, L.pad_band, swaps, rel);
+        else
+          dest_rows<NW, FORCE, RULE, 0, 1>(sl, stage, cx, lane, y0 + r, &stmap1, &padmap1, L.w0, r + 1,
+                                           L.pad, L.padx, L.pad_band, swaps, rel);
+      }
+    }
+  };
+  rows(RA0, RA0 + nA, 0u, sbase + PG::kCtrOff);
+  if (nB > 0) {
+    asm volatile("bar.sync 1, %0;" ::"r"(PG::kCons * 32) : "memory");
+    make_keys(bA + 1, threadIdx.x, PG::kCons * 32);
+    asm volatile("bar.sync 1, %0;" ::"r"(PG::kCons * 32) : "memory");
+    set_band(bA + 1);
+    rows(row_lo, row_lo + nB, offB, sbase + PG::kCtrOff + 4);
+  }
+  if (lane == 0) bulk_wait_all();
+  if (FORCE) {
+    unsigned long long sw = swaps;
+    for (int o = 16; o; o >>= 1) sw += __shfl_xor_sync(kFull, sw, o);
+    if (lane == 0 && sw) atomicAdd(a.swaps, sw);
+  }
+}
+
+// Grid of the ring / pair kernels: nbands x segment groups of the row range
+// (plus the second range's segments), with the SMs left over by nbands x
+// segment groups (148 - 8 x 18 = 4 at W = 16384) taking the last rows of two
+// bands each, so that every SM has the same work: x rows per band go to them,
+// x(2S + 1) = rows - S b with b rows of equivalent cost for their mid-kernel
+// band switch.
+template <int NW>
+int ring_grid(StepArgs& a, int num_sms) {
+  using G = Geo<NW, false>;
   const int rows = a.row_hi - a.row_lo;
   a.k4 = 4u;
   a.nbands = a.W / G::kBandCols;
@@ -1010,10 +1523,6 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
   a.segs2 = (rows2 + seg - 1) / seg;
   a.extra_rows = 0;
   int grid = a.nbands * (seg_groups + a.segs2);
-  // SMs left over by nbands x segment groups (148 - 8 x 18 = 4 at W = 16384)
-  // take the last rows of two bands each, so that every SM has the same work:
-  // x rows per band go to them, x(2S + 1) = rows - S b with b rows of
-  // equivalent cost for their mid-kernel band switch.
   const int spare = num_sms - a.nbands * (num_sms / a.nbands);
   if (FHPG_EXTRA_CTAS && rows2 == 0 && a.nbands % 2 == 0 && 2 * spare >= a.nbands &&
       num_sms / a.nbands >= 2) {
@@ -1027,26 +1536,52 @@ void launch_ring(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t 
       grid = a.nbands * a.segs1 + a.nbands / 2;
     }
   }
-  ensure_smem_optin(reinterpret_cast<const void*>(step_ring_kernel<NW, FORCE, RULE>), RG::kSmem);
+  return grid;
+}
+
+// Launch with programmatic dependent launch: the next step's grid is
+// launched while this one runs and its CTAs take SMs as they free up
+// (griddepcontrol.wait in the kernel orders every read of the previous
+// step's output).
+template <typename K, typename... Args>
+void launch_pdl(K kernel, int grid, int threads, int smem, cudaStream_t st, Args... args) {
 #if FHPG_PDL
-  // Programmatic dependent launch: the next step's grid is launched while
-  // this one runs and its CTAs take SMs as they free up (griddepcontrol.wait
-  // in the kernel orders every read of the previous step's output).
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(RG::kThreads);
-  cfg.dynamicSmemBytes = RG::kSmem;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, step_ring_kernel<NW, FORCE, RULE>, a, maps[0], maps[1], maps[2], maps[3]);
+  cudaLaunchKernelEx(&cfg, kernel, args...);
 #else
-  step_ring_kernel<NW, FORCE, RULE><<<grid, RG::kThreads, RG::kSmem, st>>>(a, maps[0], maps[1], maps[2],
-                                                                     maps[3]);
+  kernel<<<grid, threads, smem, st>>>(args...);
 #endif
+}
+
+// maps: [0] row loads, [1] band stores, [2] pad stores, [3] 4-row loads,
+// [4] 2-row band stores, [5] 2-row pad stores (make_planes_map kinds).
+template <int NW, bool FORCE, int RULE>
+void launch_ring(StepArgs a, const CUtensorMap* src, const CUtensorMap* dst, int num_sms,
+                 cudaStream_t st) {
+  using RG = RingGeo<NW, FORCE>;
+  const int grid = ring_grid<NW>(a, num_sms);
+  ensure_smem_optin(reinterpret_cast<const void*>(step_ring_kernel<NW, FORCE, RULE>), RG::kSmem);
+  launch_pdl(step_ring_kernel<NW, FORCE, RULE>, grid, RG::kThreads, RG::kSmem, st, a, src[0],
+             dst[1], dst[2], src[3]);
+}
+
+template <int NW, bool FORCE, int RULE>
+void launch_pair(StepArgs a, const CUtensorMap* src, const CUtensorMap* dst, int num_sms,
+                 cudaStream_t st) {
+  using PG = PairGeo<NW, FORCE>;
+  const int grid = ring_grid<NW>(a, num_sms);
+  ensure_smem_optin(reinterpret_cast<const void*>(step_pair_kernel<NW, FORCE, RULE>), PG::kSmem);
+  launch_pdl(step_pair_kernel<NW, FORCE, RULE>, grid, PG::kThreads, PG::kSmem, st, a, src[3],
+             dst[1], dst[2], dst[4], dst[5]);
 }
 
 template <int NW, bool FORCE>
@@ -1056,7 +1591,8 @@ int smem_bytes(int bpc) {
 }
 
 template <int NW, bool FORCE, int RULE>
-void launch_nw(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st) {
+void launch_nw(StepArgs a, const CUtensorMap* src, const CUtensorMap* dst, int num_sms,
+               cudaStream_t st) {
   using G = Geo<NW, FORCE>;
   const int rows = a.row_hi - a.row_lo;
   a.k4 = 4u;
@@ -1093,9 +1629,9 @@ void launch_nw(StepArgs a, const CUtensorMap* maps, int num_sms, cudaStream_t st
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, step_planes_kernel<NW, FORCE, RULE>, a, maps[0], maps[1], maps[2]);
+  cudaLaunchKernelEx(&cfg, step_planes_kernel<NW, FORCE, RULE>, a, src[0], dst[1], dst[2]);
 #else
-  step_planes_kernel<NW, FORCE, RULE><<<grid, kWarps * 32, smem, st>>>(a, maps[0], maps[1], maps[2]);
+  step_planes_kernel<NW, FORCE, RULE><<<grid, kWarps * 32, smem, st>>>(a, src[0], dst[1], dst[2]);
 #endif
 }
 
@@ -1205,15 +1741,18 @@ bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows,
   // Tensor {padded words, planes, rows}. Boxes: kind 0 (load) one band of
   // 32 NW words + 4 on each side, all 8 planes; kind 1 (store) the band's
   // words, planes 0-6; kind 2 (pad store) 4 words, planes 0-6; kind 3 (load)
-  // as kind 0 for two consecutive rows.
+  // as kind 0 for FHPG_BOX_ROWS consecutive rows; kinds 4 / 5 as 1 / 2 for
+  // two consecutive rows.
   const int nw = planes_words_per_lane(W);
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(W / 32 + 8), 8,
                               static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>((W / 32 + 8) * 4),
                                  static_cast<cuuint64_t>(pitch)};
+  const bool load = kind == 0 || kind == 3;
+  const bool band = kind == 1 || kind == 4;
   const cuuint32_t box[3] = {
-      static_cast<cuuint32_t>(kind == 0 || kind == 3 ? 32 * nw + 8 : kind == 1 ? 32 * nw : 4),
-      kind == 0 || kind == 3 ? 8u : 7u, kind == 3 ? static_cast<cuuint32_t>(FHPG_BOX_ROWS) : 1u};
+      static_cast<cuuint32_t>(load ? 32 * nw + 8 : band ? 32 * nw : 4), load ? 8u : 7u,
+      kind == 3 ? static_cast<cuuint32_t>(FHPG_BOX_ROWS) : (kind >= 4 ? 2u : 1u)};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode(static_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
                             buffer, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1222,32 +1761,34 @@ bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows,
   return r == CUDA_SUCCESS;
 }
 
-int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap_dst_store,
-                       const void* tmap_dst_pad, const void* tmap_src_pair, int num_sms,
-                       cudaStream_t st) {
+int launch_step_planes(const StepArgs& a, const void* src_maps, const void* dst_maps,
+                       int num_sms, cudaStream_t st) {
   const int nw = planes_words_per_lane(a.W);
   const bool force = a.thr != 0;
-  const CUtensorMap m[4] = {*static_cast<const CUtensorMap*>(tmap_src),
-                            *static_cast<const CUtensorMap*>(tmap_dst_store),
-                            *static_cast<const CUtensorMap*>(tmap_dst_pad),
-                            *static_cast<const CUtensorMap*>(tmap_src_pair)};
+  const CUtensorMap* src = static_cast<const CUtensorMap*>(src_maps);
+  const CUtensorMap* dst = static_cast<const CUtensorMap*>(dst_maps);
   // a.rule: 2 = FHP-III, 1 = FHP-I, 0 = DEFAULT (the circuit the kernels instantiate)
   auto ring = [&](auto rule) {
     constexpr int R = decltype(rule)::value;
-    if (force) launch_ring<2, true, R>(a, m, num_sms, st);
-    else launch_ring<2, false, R>(a, m, num_sms, st);
+#if FHPG_PAIR
+    if (force) launch_pair<2, true, R>(a, src, dst, num_sms, st);
+    else launch_pair<2, false, R>(a, src, dst, num_sms, st);
+#else
+    if (force) launch_ring<2, true, R>(a, src, dst, num_sms, st);
+    else launch_ring<2, false, R>(a, src, dst, num_sms, st);
+#endif
   };
   auto nwk = [&](auto rule) {
     constexpr int R = decltype(rule)::value;
     if (nw == 4) {
-      if (force) launch_nw<4, true, R>(a, m, num_sms, st);
-      else launch_nw<4, false, R>(a, m, num_sms, st);
+      if (force) launch_nw<4, true, R>(a, src, dst, num_sms, st);
+      else launch_nw<4, false, R>(a, src, dst, num_sms, st);
     } else if (nw == 2) {
-      if (force) launch_nw<2, true, R>(a, m, num_sms, st);
-      else launch_nw<2, false, R>(a, m, num_sms, st);
+      if (force) launch_nw<2, true, R>(a, src, dst, num_sms, st);
+      else launch_nw<2, false, R>(a, src, dst, num_sms, st);
     } else {
-      if (force) launch_nw<1, true, R>(a, m, num_sms, st);
-      else launch_nw<1, false, R>(a, m, num_sms, st);
+      if (force) launch_nw<1, true, R>(a, src, dst, num_sms, st);
+      else launch_nw<1, false, R>(a, src, dst, num_sms, st);
     }
   };
 #if FHPG_PLANES_RING
@@ -1263,10 +1804,8 @@ int launch_step_planes(const StepArgs& a, const void* tmap_src, const void* tmap
     a1.row_lo2 = a1.row_hi2 = a2.row_lo2 = a2.row_hi2 = 0;
     a2.row_lo = a.row_lo2;
     a2.row_hi = a.row_hi2;
-    return launch_step_planes(a1, tmap_src, tmap_dst_store, tmap_dst_pad, tmap_src_pair, num_sms,
-                              st) +
-           launch_step_planes(a2, tmap_src, tmap_dst_store, tmap_dst_pad, tmap_src_pair, num_sms,
-                              st);
+    return launch_step_planes(a1, src_maps, dst_maps, num_sms, st) +
+           launch_step_planes(a2, src_maps, dst_maps, num_sms, st);
   }
   if (a.rule == 0) nwk(std::integral_constant<int, 0>{});
   else if (a.rule == 1) nwk(std::integral_constant<int, 1>{});

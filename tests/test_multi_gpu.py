@@ -162,12 +162,14 @@ def _cuda_worker(rank, world, port_num, W, H, steps, seed, fp, init, q):
             eng.upload(state[rb:re])
         strips = DistStrips(eng, rank, world, staging="host")
         swaps = strips.advance(seed, P.bernoulli_threshold(fp), 0, steps)
-        mine = torch.from_numpy(eng.download())
         sizes = [b - a for a, b in strip_rows(H, world)]
+        mine = torch.zeros((max(sizes), W), dtype=torch.uint8)  # gloo gathers equal sizes
+        mine[: re - rb] = torch.from_numpy(eng.download())
         if rank == 0:
-            parts = [torch.empty((k, W), dtype=torch.uint8) for k in sizes]
+            parts = [torch.empty((max(sizes), W), dtype=torch.uint8) for _ in sizes]
             dist.gather(mine, parts, dst=0)
-            q.put(("ok", torch.cat(parts).numpy(), swaps))
+            rows = torch.cat([p[:k] for p, k in zip(parts, sizes)])
+            q.put(("ok", rows.numpy(), swaps))
         else:
             dist.gather(mine, None, dst=0)
         eng.close()
