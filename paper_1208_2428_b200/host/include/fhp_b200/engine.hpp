@@ -29,6 +29,9 @@ class Engine {
  public:
   Engine(int width, int height);                                     // whole lattice
   Engine(int width, int height, int row_begin, int row_end, int device);  // row strip
+  // Whole lattice in `strips` row strips, strip i on devices[i] (empty: GPU
+  // i); the library exchanges the halo rows (fhpg_create_multi).
+  Engine(int width, int height, int strips, const std::vector<int>& devices);
   ~Engine();
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -63,12 +66,18 @@ class Engine {
   std::int64_t total_mass() const;
   MomentumVec total_momentum() const;
   CellSums cell_sums(int block) const;
+  // The same sums without blocking: request_cells enqueues the reduction
+  // behind the steps already enqueued; collect_cells waits for it.
+  void request_cells(int block);
+  CellSums collect_cells();
+  int strips() const;
   // Per interior row r (index r-1): px sum over fluid nodes, fluid count.
   void row_sums(std::vector<std::int64_t>& px, std::vector<std::int32_t>& fluid) const;
 
  private:
   fhpg_engine* h_ = nullptr;
   int width_ = 0, height_ = 0, row_begin_ = 0, row_end_ = 0;
+  int cells_block_ = 0;
 };
 
 }  // namespace fhp_b200

@@ -10,6 +10,7 @@
 #include "fhp_b200/config.hpp"
 #include "fhp_b200/engine.hpp"
 #include "fhp_b200/lattice.hpp"
+#include "fhp_b200/observables.hpp"
 
 namespace fhp_b200 {
 
@@ -47,5 +48,12 @@ using DeviceDumpFn = std::function<void(int step, const Engine&)>;
 RunResult run(const SimConfig& cfg, const CollisionTable& table, const DumpFn& dump = {},
               const DeviceDumpFn& device_dump = {});
 RunResult run(const SimConfig& cfg);
+
+// run() with asynchronous coarse-grain dumps: every dump_every steps (and at
+// the end) fn gets the coarse_grain(block) field of that step; the sums are
+// reduced on the device and copied back while the next chunk of steps runs.
+using CellDumpFn = std::function<void(int step, const FlowField& field)>;
+RunResult run_cell_dumps(const SimConfig& cfg, const CollisionTable& table, int block,
+                         const CellDumpFn& fn);
 
 }  // namespace fhp_b200

@@ -23,6 +23,13 @@ Engine::Engine(int width, int height, int row_begin, int row_end, int device)
   check_status(fhpg_create_strip(width, height, row_begin, row_end, device, &h_));
 }
 
+Engine::Engine(int width, int height, int strips, const std::vector<int>& devices)
+    : width_(width), height_(height), row_end_(height) {
+  if (!devices.empty() && static_cast<int>(devices.size()) != strips)
+    throw std::invalid_argument("devices must list one GPU index per strip");
+  check_status(fhpg_create_multi(width, height, strips, devices.empty() ? nullptr : devices.data(), &h_));
+}
+
 Engine::~Engine() { fhpg_destroy(h_); }
 
 Engine::Engine(Engine&& o) noexcept { *this = std::move(o); }
@@ -35,6 +42,7 @@ Engine& Engine::operator=(Engine&& o) noexcept {
     height_ = o.height_;
     row_begin_ = o.row_begin_;
     row_end_ = o.row_end_;
+    cells_block_ = o.cells_block_;
   }
   return *this;
 }
@@ -124,6 +132,32 @@ CellSums Engine::cell_sums(int block) const {
   check_status(fhpg_reduce_cells(h_, block, s.nodes.data(), s.particles.data(), s.px.data(),
                                  s.py.data()));
   return s;
+}
+
+void Engine::request_cells(int block) {
+  check_status(fhpg_reduce_cells_async(h_, block));
+  cells_block_ = block;
+}
+
+CellSums Engine::collect_cells() {
+  if (cells_block_ < 1) throw std::invalid_argument("no coarse-grain request pending");
+  CellSums s;
+  s.cells_x = (width_ + cells_block_ - 1) / cells_block_;
+  s.cells_y = (height_ - 2 + cells_block_ - 1) / cells_block_;
+  const std::size_t n = static_cast<std::size_t>(s.cells_x) * s.cells_y;
+  s.nodes.assign(n, 0);
+  s.particles.assign(n, 0);
+  s.px.assign(n, 0);
+  s.py.assign(n, 0);
+  if (n) check_status(fhpg_cells_wait(h_, s.nodes.data(), s.particles.data(), s.px.data(), s.py.data()));
+  cells_block_ = 0;
+  return s;
+}
+
+int Engine::strips() const {
+  int n = 1;
+  check_status(fhpg_strips(h_, &n, nullptr, nullptr, nullptr));
+  return n;
 }
 
 void Engine::row_sums(std::vector<std::int64_t>& px, std::vector<std::int32_t>& fluid) const {

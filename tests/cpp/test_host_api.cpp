@@ -157,6 +157,18 @@ static void cpu_tests() {
   cfg = SimConfig{};
   cfg.lanes = 33;
   CHECK_THROWS_AS(cfg.validate(), std::invalid_argument);
+  cfg = SimConfig{};
+  cfg.gpus = 0;
+  CHECK_THROWS_AS(cfg.validate(), std::invalid_argument);
+  cfg = SimConfig{};
+  cfg.gpus = 2;
+  cfg.devices = {0};
+  CHECK_THROWS_AS(cfg.validate(), std::invalid_argument);
+  cfg = SimConfig{};
+  cfg.height = 5;
+  cfg.gpus = 4;  // 3 interior rows (make_strip_plan)
+  CHECK_THROWS_AS(cfg.validate(), std::invalid_argument);
+  CHECK(std::string(backend_name(Backend::Cuda)) == "cuda");
   CHECK(compute_mups(1000, 1000, 100, 0.1) == 1000.0);
   CHECK_THROWS_AS(compute_mups(1, 1, 1, 0.0), std::invalid_argument);
   BenchRecord rec;
@@ -273,6 +285,59 @@ static void gpu_tests() {
     CHECK(peq);
     CHECK(total_mass(e) == total_mass(res.lattice));
     CHECK(total_momentum(e) == total_momentum(res.lattice));
+  }
+  // cfg.gpus: the same run over 3 row strips (all on device 0 here), and the
+  // asynchronous cell-dump pipeline: identical lattice, swaps and dumps
+  {
+    SimConfig c;
+    c.width = 2048;
+    c.height = 131;
+    c.steps = 50;
+    c.fill_density = 0.25;
+    c.force_p = 0.02;
+    c.seed = 21;
+    c.dump_every = 20;
+    c.rules = RuleVariant::FhpIII;
+    const auto table = build_table(RuleVariant::FhpIII);
+    std::vector<FlowField> sync_dumps;
+    const auto one = run(c, table, {}, [&](int, const Engine& e) { sync_dumps.push_back(coarse_grain(e, 16)); });
+    SimConfig c3 = c;
+    c3.gpus = 3;
+    c3.devices = {0, 0, 0};
+    std::vector<int> steps_seen;
+    std::vector<FlowField> async_dumps;
+    const auto three = run_cell_dumps(c3, table, 16, [&](int s, const FlowField& f) {
+      steps_seen.push_back(s);
+      async_dumps.push_back(f);
+    });
+    CHECK(interior(three.lattice) == interior(one.lattice));
+    CHECK(three.forcing_swaps == one.forcing_swaps);
+    CHECK((steps_seen == std::vector<int>{20, 40, 50}));
+    bool same = async_dumps.size() == sync_dumps.size();
+    for (size_t k = 0; same && k < async_dumps.size(); ++k)
+      for (size_t i = 0; same && i < async_dumps[k].cells.size(); ++i)
+        same = async_dumps[k].cells[i].rho == sync_dumps[k].cells[i].rho &&
+               async_dumps[k].cells[i].ux == sync_dumps[k].cells[i].ux &&
+               async_dumps[k].cells[i].uy == sync_dumps[k].cells[i].uy;
+    CHECK(same);
+    CHECK(three.series.size() == one.series.size() &&
+          three.series.back().mass == one.series.back().mass);
+    // the drop-in keeps its engine between calls; a new table is picked up
+    std::vector<uint8_t> s0, m0;
+    Lattice lat = scrambled(2048, 40, 99, s0, m0);
+    SimConfig cd;
+    cd.seed = 5;
+    cd.force_p = 0.1;
+    uint64_t sw = advance(lat, table, cd, 0, 4);
+    const auto tdef = build_table(RuleVariant::Default);
+    sw += advance(lat, tdef, cd, 4, 3);
+    std::vector<uint8_t> ref = s0;
+    uint64_t rsw = fo_advance(2048, 40, ref.data(), m0.data(), table.entries.data(), cd.seed,
+                              fo_bernoulli_threshold(cd.force_p), 0, 4);
+    rsw += fo_advance(2048, 40, ref.data(), m0.data(), tdef.entries.data(), cd.seed,
+                      fo_bernoulli_threshold(cd.force_p), 4, 3);
+    CHECK(interior(lat) == ref);
+    CHECK(sw == rsw);
   }
   // run_bench with an injected clock (acceptance.cpp:239-258)
   {
