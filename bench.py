@@ -58,6 +58,44 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def int_roof(table, peak_bw_gbs):
+    """SURVEY 8(d)'s second roof: integer ops per site at the INT32 peak.
+    Algorithmic ops = 22 (one mix64 on sm_100a) x (f_chir + f_force): the
+    chirality / forcing draws the path cannot avoid; f_chir exact for i.i.d.
+    density-d states (each chirality slice of the table is a permutation, so
+    states stay i.i.d.), f_force = 0 at p = 0. The peak is the measured
+    half-rate LOP3/SHF/IMAD lane rate (profiles/int_peaks_r01.json). The
+    implementation's own ALU-pipe instructions per site (ncu, when the
+    committed summary has them) give the roof this kernel actually faces."""
+    d = DENSITY
+    f_chir = 0.0
+    for st in range(128):
+        if table[st] != table[256 + st]:
+            k = bin(st).count("1")
+            f_chir += d ** k * (1 - d) ** (7 - k)
+    f_force = d * (1 - d) if FORCE_P > 0 else 0.0
+    ops = 22.0 * (f_chir + f_force)
+    peak = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "int_peaks_r01.json")) as f:
+            peak = float(json.load(f)["kernels"]["lop3"]["lane_ops_per_s"])
+    except Exception:
+        peak = 148 * 64 * 1.965e9  # half-rate INT pipe at the max SM clock
+    out = {"ops_per_site": ops, "f_chir": f_chir, "f_force": f_force,
+           "peak_lane_ops_per_s": peak, "roof_gsups": peak / ops / 1e9,
+           "hbm_roof_gsups": peak_bw_gbs / BYTES_PER_SITE}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_step_kernel.json")) as f:
+            alu = json.load(f).get("alu_inst_per_site")
+        if alu:
+            out["impl_alu_inst_per_site"] = alu
+            out["impl_alu_roof_gsups"] = peak / alu / 1e9
+    except Exception:
+        pass
+    out["bound"] = "hbm" if out["hbm_roof_gsups"] <= out["roof_gsups"] else "int"
+    return out
+
+
 def ncu_traffic():
     """dram bytes per step-kernel launch from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_step_kernel.json")
@@ -292,6 +330,7 @@ def main():
               "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                            "frac": achieved / peak, "traffic": traffic,
                            "bytes_per_site": BYTES_PER_SITE, "peak_source": peak_src,
+                           "int": int_roof(table, peak),
                            "timing": "CUDA events on the engine stream around the K-step loop, "
                                      "per-step average (one step kernel per step at N=1)"},
               "gpu_launches": gpu_launches,

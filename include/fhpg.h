@@ -72,6 +72,9 @@ int fhpg_create_strip(int width, int height, int row_begin, int row_end, int dev
 int fhpg_create_multi(int width, int height, int n_strips, const int* devices,
                       fhpg_engine** out);
 
+/* Number of CUDA devices visible to the library (for strip placement). */
+int fhpg_device_count(int* n);
+
 /* Strip layout of an engine: *n_strips (1 for a single-strip engine) and,
  * for each strip i (arrays of n_strips entries, each may be NULL), its rows
  * [row_begin[i], row_end[i]) and CUDA device. */
@@ -184,8 +187,10 @@ int fhpg_info(fhpg_engine* e, int* width, int* height, int* row_begin, int* row_
 int fhpg_force_generic(fhpg_engine* e, int on);
 
 /* Step-kernel selection: 0 = automatic (bit-plane path when the table has a
- * bit-sliced circuit — FHP-III — and W % 1024 == 0, else the byte streaming
- * path when W allows it, else generic), 1 = byte paths only, 2 = generic.
+ * bit-sliced circuit — FHP-III, FHP-I, DEFAULT — and W % 1024 == 0, with the
+ * shared-memory-resident kernel for multi-step calls on small lattices; else
+ * the byte streaming path when W allows it, else generic), 1 = byte paths
+ * only, 2 = generic, 3 = bit-plane streaming kernels only (no resident kernel).
  * The resident state is converted between layouts on the device; results
  * are identical on every path. */
 int fhpg_select_path(fhpg_engine* e, int path);

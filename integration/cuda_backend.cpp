@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 #include <stdexcept>
+#include <vector>
 
 #include "fhpg.h"
 
@@ -30,7 +31,16 @@ struct EngineCache {
     if (!engine || w != width || h != height || n != gpus) {
       engine.reset();
       fhpg_engine* e = nullptr;
-      fhpg_check(n > 1 ? fhpg_create_multi(w, h, n, nullptr, &e) : fhpg_create(w, h, &e));
+      if (n > 1) {
+        // strip i on GPU i, wrapping around when there are fewer GPUs
+        int ndev = 0;
+        fhpg_check(fhpg_device_count(&ndev));
+        std::vector<int> dev(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) dev[i] = ndev > 0 ? i % ndev : 0;
+        fhpg_check(fhpg_create_multi(w, h, n, dev.data(), &e));
+      } else {
+        fhpg_check(fhpg_create(w, h, &e));
+      }
       engine.reset(e);
       width = w;
       height = h;

@@ -28,7 +28,7 @@ struct fhpg_engine {
   bool planes = false;
   bool table_planes = false;
   int planes_rule = 2;                   // circuit of the table: FHPG_RULES_* (fhpg_tables.h)
-  int path_pref = 0;                     // 0 auto, 1 byte fast path, 2 generic
+  int path_pref = 0;                     // 0 auto, 1 byte fast path, 2 generic, 3 streaming planes
   uint8_t* scratch = nullptr;            // nrows * pitch
   alignas(64) unsigned char tmap[2][fhpg::kPlaneMaps][128];  // TMA descriptors of buf[0], buf[1] (planes)
   bool scratch_valid = false;
@@ -36,6 +36,7 @@ struct fhpg_engine {
   uint64_t* zkeys = nullptr;             // [parity][purpose][W]
   unsigned long long* swaps = nullptr;
   long long* acc = nullptr;              // reduction scratch (3)
+  unsigned* bar = nullptr;               // grid barrier of the resident kernel (2 words)
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   cudaEvent_t tail = nullptr;            // recorded after the last enqueued work (any stream)
@@ -145,6 +146,7 @@ void release(fhpg_engine* e) {
   cudaFree(e->zkeys);
   cudaFree(e->swaps);
   cudaFree(e->acc);
+  cudaFree(e->bar);
   cudaFree(e->cells_dev);
   cudaFreeHost(e->cells_host);
   if (e->cells_ev) cudaEventDestroy(e->cells_ev);
@@ -190,6 +192,8 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
     ck(cudaMalloc(&e->swaps, sizeof(unsigned long long)), "cudaMalloc(swaps)");
     ck(cudaMemset(e->swaps, 0, sizeof(unsigned long long)), "cudaMemset(swaps)");
     ck(cudaMalloc(&e->acc, sizeof(long long) * 4), "cudaMalloc(acc)");
+    ck(cudaMalloc(&e->bar, sizeof(unsigned) * 2), "cudaMalloc(bar)");
+    ck(cudaMemset(e->bar, 0, sizeof(unsigned) * 2), "cudaMemset(bar)");
     ck(cudaStreamCreateWithFlags(&e->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     e->stream = e->own_stream;
     ck(cudaEventCreateWithFlags(&e->tail, cudaEventDisableTiming), "cudaEventCreate");
@@ -205,7 +209,8 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
 }
 
 bool want_planes(const fhpg_engine* e) {
-  return e->table_set && e->table_planes && e->path_pref == 0 && fhpg::planes_ok(e->W);
+  return e->table_set && e->table_planes && (e->path_pref == 0 || e->path_pref == 3) &&
+         fhpg::planes_ok(e->W);
 }
 
 void need_scratch(fhpg_engine* e) {
@@ -282,6 +287,24 @@ void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64
     e->normalized = true;
   }
   const bool force = thr != 0;
+  // Small whole lattices: the shared-memory-resident kernel, one cooperative
+  // launch for the whole call (fhpg_step_resident.cu).
+  int rpc = 0, grid = 0;
+  if (e->planes && e->path_pref == 0 && count >= 2 && e->row_begin == 0 && e->row_end == e->H &&
+      resident_plan(e->W, e->H, thr, e->num_sms, &rpc, &grid) > 0) {
+    uint8_t* const g[2] = {e->base(0), e->base(1)};
+    cudaError_t err = cudaSuccess;
+    const int flips = launch_step_resident(g, e->cur, e->pitch, e->W, e->H, e->planes_rule, seed, thr,
+                                           first, count, e->swaps, e->bar, e->num_sms, st, &err);
+    ck(err, "resident step launch");
+    ck(cudaGetLastError(), "resident step launch");
+    e->cur ^= flips & 1;
+    e->scratch_valid = false;
+    ++e->launches;
+    e->keys_step = -1;
+    ck(cudaEventRecord(e->tail, st), "cudaEventRecord");
+    return;
+  }
   const uint64_t s0 = static_cast<uint64_t>(first);
   launch_column_keys(e->keys(s0 & 1, 0), force ? e->keys(s0 & 1, 1) : nullptr,
                      step_key(seed, kChirality, s0), step_key(seed, kForcing, s0), e->W, st);
@@ -588,6 +611,14 @@ uint64_t fhpg_digest(const uint8_t* bytes, size_t n) {
   uint64_t h = 0xCBF29CE484222325ull;
   for (size_t i = 0; i < n; ++i) h = (h ^ bytes[i]) * 0x100000001B3ull;
   return h;
+}
+
+int fhpg_device_count(int* n) {
+  return guarded([&] {
+    if (!n) invalid("null output pointer");
+    *n = 0;
+    ck(cudaGetDeviceCount(n), "cudaGetDeviceCount");
+  });
 }
 
 int fhpg_create(int width, int height, fhpg_engine** out) {
@@ -1035,7 +1066,8 @@ int fhpg_force_generic(fhpg_engine* e, int on) {
 int fhpg_select_path(fhpg_engine* e, int path) {
   return guarded([&] {
     need(e);
-    if (path < 0 || path > 2) invalid("path must be 0 (auto), 1 (byte fast path) or 2 (generic)");
+    if (path < 0 || path > 3)
+      invalid("path must be 0 (auto), 1 (byte fast path), 2 (generic) or 3 (streaming kernels only)");
     each(e, [&](fhpg_engine* p) {
       p->path_pref = path;
       sync_layout(p);

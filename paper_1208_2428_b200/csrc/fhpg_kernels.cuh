@@ -77,6 +77,18 @@ bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows,
 // kPlaneMaps descriptors of each buffer, in kind order).
 int launch_step_planes(const StepArgs& a, const void* src_maps, const void* dst_maps,
                        int num_sms, cudaStream_t st);
+// Small whole lattices (fhpg_step_resident.cu): the depth (steps per grid
+// barrier) the shared-memory-resident kernel would use for W x H, or 0 when
+// the lattice is not eligible (W % 1024, too large, shared memory).
+int resident_plan(int W, int H, uint64_t thr, int num_sms, int* rows_per_cta, int* grid);
+// `count` steps from global step `first` of a whole plane lattice held in
+// g[cur] in ONE cooperative launch; returns the number of buffer flips (the
+// state ends in g[cur ^ (flips & 1)]). `bar`: 2 zeroed words of device memory.
+int launch_step_resident(uint8_t* const g[2], int cur, size_t pitch, int W, int H, int rule,
+                         uint64_t seed, uint64_t thr, long long first, long long count,
+                         unsigned long long* swaps, unsigned* bar, int num_sms, cudaStream_t st,
+                         cudaError_t* err);
+
 // Bytes (rows 0..nrows-1 of src) -> planes in dst; plane 7 from the mask,
 // also written into dst_obst (the other ping-pong buffer).
 void launch_pack_planes(const uint8_t* src, const uint8_t* mask, uint8_t* dst, uint8_t* dst_obst,

@@ -1,0 +1,372 @@
+// fhpg_planes_dev.cuh — device helpers shared by the bit-plane kernels
+// (fhpg_step_planes.cu: the streaming ring kernels; fhpg_step_resident.cu:
+// the shared-memory-resident kernel for small lattices): shared-memory and
+// TMA / mbarrier primitives, the rule dispatch, the plane reads of the
+// hexagonal pull and the balanced chirality walk. Included inside an
+// anonymous namespace of namespace fhpg.
+#pragma once
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// Collision circuits the bit-plane kernels evaluate (fhpg_planes_rules.cuh):
+// RULE 2 = FHP-III, 1 = FHP-I, 0 = the reference's DEFAULT rule.
+template <int RULE>
+struct PlaneRule;
+template <>
+struct PlaneRule<2> {
+  using Class = Fhp3Class;
+  static __device__ __forceinline__ Class classify(const uint32_t a[6], uint32_t r, uint32_t s) {
+    return fhp3_classify(a, r, s);
+  }
+  static __device__ __forceinline__ void apply(const Class& k, uint32_t c, uint32_t r,
+                                               const uint32_t a[6], uint32_t o[6], uint32_t& o_r,
+                                               uint32_t) {
+    fhp3_apply(k, c, r, a, o, o_r);
+  }
+};
+template <>
+struct PlaneRule<1> {
+  using Class = Fhp1Class;
+  static __device__ __forceinline__ Class classify(const uint32_t a[6], uint32_t r, uint32_t s) {
+    return fhp1_classify(a, r, s);
+  }
+  static __device__ __forceinline__ void apply(const Class& k, uint32_t c, uint32_t r,
+                                               const uint32_t a[6], uint32_t o[6], uint32_t& o_r,
+                                               uint32_t s) {
+    fhp1_apply(k, c, r, a, o, o_r, s);
+  }
+};
+template <>
+struct PlaneRule<0> {
+  using Class = DefClass;
+  static __device__ __forceinline__ Class classify(const uint32_t a[6], uint32_t r, uint32_t s) {
+    return def_classify(a, r, s);
+  }
+  static __device__ __forceinline__ void apply(const Class& k, uint32_t c, uint32_t r,
+                                               const uint32_t a[6], uint32_t o[6], uint32_t& o_r,
+                                               uint32_t s) {
+    def_apply(k, c, r, a, o, o_r, s);
+  }
+};
+// Warps per CTA (one CTA per SM): 16 with 2 words per lane, 8 with 4.
+// Programmatic dependent launch of the step kernels: the next step's grid is
+// launched while this one runs (griddepcontrol.wait orders its reads).
+#ifndef FHPG_PDL
+#define FHPG_PDL 1
+#endif
+#ifndef FHPG_STREAM_ONLY
+#define FHPG_STREAM_ONLY 0  // timing experiments (wrong results): 1 memory pipeline only,
+                            // 2 loads only, 3 stores only, 4 loads + shared reads,
+                            // 5 compute + stores (no loads), 6 compute only
+#endif
+
+#ifndef FHPG_PLANES_RING
+#define FHPG_PLANES_RING 1
+#endif
+#ifndef FHPG_PLANES_WARPS
+#define FHPG_PLANES_WARPS 16
+#endif
+#ifndef FHPG_PLANES_SLOTS
+#define FHPG_PLANES_SLOTS 4
+#endif
+template <int NW>
+constexpr int kPWarps = NW == 4 ? 8 : FHPG_PLANES_WARPS;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64v(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v));
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w));
+}
+__device__ __forceinline__ void red_or(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ uint32_t top_bit(uint32_t m) {
+  uint32_t p;
+  asm("bfind.u32 %0, %1;" : "=r"(p) : "r"(m));
+  return p;
+}
+
+// mbarrier + bulk async copy (TMA engine, non-tensor form).
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  } while (!done);
+}
+// One TMA box {72 words, 8 planes, 1 row} of the plane tensor.
+__device__ __forceinline__ void tma_row(uint32_t dst, const CUtensorMap* map, int word, int row,
+                                        uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(map), "r"(word), "r"(0), "r"(row), "r"(bar) : "memory");
+}
+
+// TMA store of a dense smem box (the 7 outgoing planes of a band row, or
+// the 4 pad words of each plane) into the plane tensor; bulk-group tracked.
+__device__ __forceinline__ void tma_store(const CUtensorMap* map, int word, int row, uint32_t src) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
+      ::"l"(map), "r"(word), "r"(0), "r"(row), "r"(src) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+template <int NW>
+__device__ __forceinline__ void stsv(uint32_t a, const uint32_t (&v)[NW]) {
+  if constexpr (NW == 4) {
+    sts128(a, v[0], v[1], v[2], v[3]);
+  } else if constexpr (NW == 2) {
+    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(v[0]), "r"(v[1]));
+  } else {
+    sts32(a, v[0]);
+  }
+}
+
+template <int NW>
+__device__ __forceinline__ void stv(uint32_t* p, const uint32_t (&v)[NW]) {
+  if constexpr (NW == 4) {
+    __stcs(reinterpret_cast<uint4*>(p), make_uint4(v[0], v[1], v[2], v[3]));
+  } else if constexpr (NW == 2) {
+    __stcs(reinterpret_cast<uint2*>(p), make_uint2(v[0], v[1]));
+  } else {
+    __stcs(p, v[0]);
+  }
+}
+
+// Geometry of a warp's smem: a ring of kSlots source rows. A slot holds the
+// 8 planes of the band, each as [4 words left of the band | band words | 4
+// words right of it] (one TMA box), so the +-1 column funnel shifts read the
+// neighbouring lane's (or band's) word straight from shared memory.
+template <int NW, bool FORCE>
+struct Geo {
+  static constexpr int kBandWords = 32 * NW;
+  static constexpr int kBandCols = 1024 * NW;
+  static constexpr int kPlane = 32 + 4 * kBandWords;
+  static constexpr int kSlot = 8 * kPlane;
+  static constexpr int kSlots = FHPG_PLANES_SLOTS;
+  // Output staging (7 planes x band words, the TMA store source) followed by
+  // the two pad boxes (7 x 4 words each). The walk's list and result words
+  // reuse the staging area: they are dead before the row's outputs land.
+  static constexpr int kStage = 7 * 4 * kBandWords;
+  static constexpr int kPadL = kStage, kPadR = kStage + 128;  // TMA sources: 128 B aligned
+  static constexpr int kList = 16 * kBandWords;   // walk list entries (uint4), inside the stage
+  static constexpr int kOut = 4 * kBandWords;     // walk result words, after the list
+  static_assert(kList + kOut <= kStage + 240, "walk scratch must fit the staging area");
+  static_assert(kStage % 128 == 0, "TMA store sources are 128 B aligned");
+  static constexpr int kStageAll = kStage + 256;
+  static constexpr int kWarp = (kSlots * kSlot + kStageAll + 8 * kSlots + 127) / 128 * 128;
+  static constexpr uint32_t kRowBytes = kSlot;
+};
+
+struct Lanes {
+  int lane;
+  int WW;           // words per plane row (W / 32)
+  int PW;           // words per padded plane row (W / 32 + 8)
+  int w0;           // first word of the band
+  int pad;          // this lane's words also go to this pad staging offset (-1: none)
+  int padx;         // bit 0: left pad box, bit 1: right pad box (word WW + 4 = (padx >> 2) + 4)
+  bool pad_band;    // warp-uniform: some lane of the band writes a pad
+};
+
+// Plane words of this lane from a slot: aligned, or shifted by one column.
+template <int NW>
+__device__ __forceinline__ void rd_al(uint32_t a, uint32_t (&o)[NW]) {
+  if constexpr (NW == 4) {
+    const uint4 v = lds128(a);
+    o[0] = v.x;
+    o[1] = v.y;
+    o[2] = v.z;
+    o[3] = v.w;
+  } else if constexpr (NW == 2) {
+    const uint2 v = lds64v(a);
+    o[0] = v.x;
+    o[1] = v.y;
+  } else {
+    o[0] = lds32(a);
+  }
+}
+// L: out bit j = column x-1 (funnel with the previous word).
+template <int NW>
+__device__ __forceinline__ void rd_shl(uint32_t a, uint32_t (&o)[NW]) {
+  uint32_t v[NW];
+  rd_al<NW>(a, v);
+  const uint32_t prev = lds32(a - 4);
+  o[0] = __funnelshift_l(prev, v[0], 1);
+#pragma unroll
+  for (int i = 1; i < NW; ++i) o[i] = __funnelshift_l(v[i - 1], v[i], 1);
+}
+// R: out bit j = column x+1 (funnel with the next word).
+template <int NW>
+__device__ __forceinline__ void rd_shr(uint32_t a, uint32_t (&o)[NW]) {
+  uint32_t v[NW];
+  rd_al<NW>(a, v);
+  const uint32_t next = lds32(a + 4 * NW);
+#pragma unroll
+  for (int i = 0; i < NW - 1; ++i) o[i] = __funnelshift_r(v[i], v[i + 1], 1);
+  o[NW - 1] = __funnelshift_r(v[NW - 1], next, 1);
+}
+
+// Balanced walk over the set bits of the warp's NW * 32 mask words (word
+// i = lane * NW + w <-> band word i, bit j <-> column 32 i + j of the band).
+// The warp's nonzero words go to a list {mask, key address of the word's
+// first column, sites before it, result word address}; the T sites are
+// split into 32 equal contiguous slices; each lane finds its first word
+// (binary search over the lanes' counts), skips the sites before its slice
+// and visits its sites, advancing through the list (it has no empty words).
+// fn(key address) returns the site's result bit, ORed into the result
+// words (osm). Returns T.
+template <int NW, typename Fn>
+__device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint32_t osm,
+                                    uint32_t keys, int lane, Fn&& fn) {
+  int cnt = 0, nz = 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    cnt += __popc(m[w]);
+    nz += m[w] != 0u;
+  }
+  const int packed = cnt | (nz << 16);
+  int incl = packed;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(kFull, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const int T = __shfl_sync(kFull, incl, 31) & 0xFFFF;
+  if (T == 0) return 0;
+  const int excl = incl - packed;
+  {
+    int q = excl >> 16, c = excl & 0xFFFF;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      if (m[w]) {
+        const uint32_t wi = static_cast<uint32_t>(lane * NW + w);
+        sts128(lsm + q * 16, m[w], keys + wi * 256u, static_cast<uint32_t>(c), osm + wi * 4u);
+        ++q;
+        c += __popc(m[w]);
+      }
+      sts32(osm + (lane * NW + w) * 4, 0u);
+    }
+  }
+  __syncwarp();
+  const int s = (lane * T) >> 5;
+  const int e = ((lane + 1) * T) >> 5;
+  // owner lane of site s: last lane whose exclusive count is <= s
+  const int icnt = incl & 0xFFFF;
+  int o = 0;
+#pragma unroll
+  for (int step = 16; step; step >>= 1) {
+    const int v = __shfl_sync(kFull, icnt, o + step - 1);
+    if (v <= s) o += step;
+  }
+  const int o_excl = __shfl_sync(kFull, excl, o);
+  if (s < e) {
+    uint32_t qa = lsm + (o_excl >> 16) * 16u;  // list entry address
+    uint4 en = lds128(qa);
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      if (s >= static_cast<int>(en.z) + __popc(en.x)) {
+        qa += 16u;
+        en = lds128(qa);
+      }
+    }
+    // Sites are visited lowest bit first (measured a little faster than top
+    // bit first): skip the slice's predecessors.
+    uint32_t mask = en.x, kw = en.y, ow = en.w;
+    for (int k = s - static_cast<int>(en.z); k > 0; --k) mask &= mask - 1u;
+    // site: key address, result word address, bit index
+    // j: bit index, v: 1 << j (the result bit's placement is an IMAD with
+    // v, FMA pipe, where a shift by j would take the ALU pipe)
+    auto next = [&](uint32_t& ka, uint32_t& wa, uint32_t& v) {
+      if (mask == 0u) {
+        qa += 16u;
+        const uint4 n = lds128(qa);
+        mask = n.x;
+        kw = n.y;
+        ow = n.w;
+      }
+      v = mask & (0u - mask);
+      mask ^= v;
+      ka = kw + top_bit(v) * 8u;
+      wa = ow;
+    };
+    int it = s;
+    for (; it + 1 < e; it += 2) {
+      uint32_t k0, w0, v0, k1, w1, v1;
+      next(k0, w0, v0);
+      next(k1, w1, v1);
+      const uint32_t b0 = fn(k0), b1 = fn(k1);
+      red_or(w0, b0 * v0);
+      red_or(w1, b1 * v1);
+    }
+    if (it < e) {
+      uint32_t k0, w0, v0;
+      next(k0, w0, v0);
+      red_or(w0, fn(k0) * v0);
+    }
+  }
+  __syncwarp();
+  return T;
+}
+
+template <int NW, bool FORCE>
+struct Ctx {
+  uint32_t kc;      // smem: chirality keys of the band (8 B per column)
+  uint32_t kf;      // smem: forcing keys of the band (8 B per column)
+  uint32_t four;    // 4, passed at run time (chir_bit)
+  uint32_t lsm;     // smem: walk list
+  uint32_t osm;     // smem: walk result words
+  uint32_t stage;   // smem: output staging (the TMA store source)
+  uint64_t thr;
+};
+
+// One destination row. sm, sc, sn: this lane's word address inside plane 0
+// of the slots of rows r-1, r, r+1; Q = global parity of r.
+// `released()` is called once the source rows have been read into
+// registers (the ring slots may be refilled from then on).

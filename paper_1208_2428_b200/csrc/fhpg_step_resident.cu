@@ -1,0 +1,293 @@
+// fhpg_step_resident.cu — small bit-plane lattices (cfg1: 1024 x 1024): a
+// whole advance call in ONE cooperative launch, the lattice held in shared
+// memory, time-blocked with deep halos.
+//
+// At 1M sites a step is ~0.5 us of work but a launch of the streaming ring
+// kernel costs ~5 us (grid start, ring fill, drain; profiles/height_r01h.json)
+// — the small BASELINE shape is launch-bound. Here each CTA owns a band of
+// rows [r0, r1) of the whole lattice and works in blocks of k steps: it loads
+// rows [r0 - k, r1 + k) (all 8 planes, with the periodic-wrap pad words) into
+// shared memory, computes k steps there on a shrinking row range (row r of
+// step j needs rows r-1..r+1 of step j-1, so after k steps exactly [r0, r1) is
+// valid; rows outside the lattice stay zero, the reference's out-of-grid
+// rows, step.cpp:47), writes [r0, r1) back to the other global buffer and
+// meets the other CTAs at a grid barrier — one barrier and one L2 round trip
+// per k steps instead of a launch per step. The halo rows are recomputed by
+// the neighbouring CTAs; every random decision is keyed by global (x, y,
+// step), so the redundant copies are bit-identical and the result is the
+// streaming kernels' (and the reference's) exactly.
+//
+// Per destination row and 1024-column band, one warp evaluates the same
+// pull / circuit / lazy-chirality walk as the ring kernel (fhpg_planes_dev.cuh,
+// fhpg_planes_rules.cuh), reading and writing shared memory only.
+#include <cstdint>
+#include <type_traits>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "fhpg_common.cuh"
+#include "fhpg_kernels.cuh"
+#include "fhpg_planes_rules.cuh"
+
+namespace fhpg {
+namespace {
+
+#include "fhpg_planes_dev.cuh"
+
+constexpr int kResWarps = 16;
+constexpr int kResThreads = kResWarps * 32;
+constexpr int kResScratch = 16 * 32 + 4 * 32;  // walk list (32 entries) + result words (32)
+
+struct ResArgs {
+  uint8_t* g0;             // the engine's two plane buffers, local row 0
+  uint8_t* g1;
+  int cur;                 // buffer holding the state at `first`
+  size_t pitch;
+  int W, H;
+  int rows_per_cta;
+  int depth;               // k: steps per block (halo depth)
+  long long first, count;  // global step indices first .. first + count - 1
+  uint64_t seed, thr;
+  uint32_t k4;             // 4, at run time (chir_bit)
+  unsigned long long* swaps;
+  unsigned* bar;           // grid barrier: [0] arrivals, [1] generation
+};
+
+__device__ __forceinline__ uint4 ldcg128(const void* p) {
+  return __ldcg(reinterpret_cast<const uint4*>(p));  // L2 only: other SMs wrote it
+}
+
+// All CTAs of the (cooperative) grid: every global store issued before the
+// barrier is visible to every load issued after it.
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned gen;
+    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      for (;;) {
+        unsigned now;
+        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(now) : "l"(bar + 1) : "memory");
+        if (now != gen) break;
+        __nanosleep(32);
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// One destination row (parity Q) of one band: sm, sc, sn = this lane's word
+// in plane 0 of rows r-1, r, r+1 of the source buffer; dst = the same word of
+// row r in the destination buffer; P = plane stride (bytes); pad = byte
+// offset of this word's periodic-wrap copy (0: none).
+template <int RULE, bool FORCE, int Q>
+__device__ __forceinline__ void resident_row(uint32_t sm, uint32_t sc, uint32_t sn, uint32_t dst,
+                                             uint32_t P, int pad, uint32_t kc, uint32_t kf,
+                                             uint32_t lsm, uint32_t osm, int lane, uint32_t y,
+                                             uint32_t four, uint64_t thr, bool own, unsigned& swaps) {
+  uint32_t a0[1], a1[1], a2[1], a3[1], a4[1], a5[1], rr[1], so[1];
+  // Pull sources (backends.cpp:64-73): k0 (x+q, r+1), k1 (x+q-1, r+1),
+  // k2 (x-1, r), k3 (x+q-1, r-1), k4 (x+q, r-1), k5 (x+1, r).
+  if (Q) rd_shr<1>(sn + 0 * P, a0); else rd_al<1>(sn + 0 * P, a0);
+  if (Q) rd_al<1>(sn + 1 * P, a1); else rd_shl<1>(sn + 1 * P, a1);
+  rd_shl<1>(sc + 2 * P, a2);
+  if (Q) rd_al<1>(sm + 3 * P, a3); else rd_shl<1>(sm + 3 * P, a3);
+  if (Q) rd_shr<1>(sm + 4 * P, a4); else rd_al<1>(sm + 4 * P, a4);
+  rd_shr<1>(sc + 5 * P, a5);
+  rd_al<1>(sc + 6 * P, rr);
+  rd_al<1>(sc + 7 * P, so);
+  const uint32_t a[6] = {a0[0], a1[0], a2[0], a3[0], a4[0], a5[0]};
+  const auto K = PlaneRule<RULE>::classify(a, rr[0], so[0]);
+  const uint32_t dep[1] = {K.dep};
+  // chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y) (step.cpp:73-76)
+  const int T = walk<1>(dep, lsm, osm, kc, lane,
+                        [&](uint32_t ka) { return chir_bit(lds64(ka) + y, four); });
+  const uint32_t c = T ? lds32(osm + lane * 4) : 0u;
+  uint32_t o[7];
+  PlaneRule<RULE>::apply(K, c, rr[0], a, o, o[6], so[0]);
+  if constexpr (FORCE) {
+    // step.cpp:79-88: fluid, W (bit 5) set, E (bit 2) clear after collision
+    const uint32_t f[1] = {~so[0] & o[5] & ~o[2]};
+    const int TF = walk<1>(f, lsm, osm, kf, lane, [&](uint32_t ka) {
+      return (fin64(lds64(ka) + y) >> 32) < thr ? 1u : 0u;
+    });
+    if (TF) {
+      const uint32_t acc = lds32(osm + lane * 4);
+      o[5] ^= acc;
+      o[2] ^= acc;
+      if (own) swaps += __popc(acc);  // halo rows are counted by their owner CTA
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < 7; ++p) sts32(dst + p * P, o[p]);
+  sts32(dst + 7 * P, so[0]);  // the obstacle plane travels with the row
+  if (pad) {
+#pragma unroll
+    for (int p = 0; p < 7; ++p) sts32(dst + p * P + pad, o[p]);
+    sts32(dst + 7 * P + pad, so[0]);
+  }
+}
+
+template <int RULE, bool FORCE>
+__global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int WW = a.W >> 5;
+  const uint32_t P = static_cast<uint32_t>(WW + 8) * 4u;  // plane row (pads included)
+  const uint32_t RB = 8u * P;                              // row of 8 planes
+  const int nb = a.W >> 10;                                // 1024-column bands
+  const int k = a.depth;
+  const int r0 = blockIdx.x * a.rows_per_cta, r1 = min(a.H, r0 + a.rows_per_cta);
+  const int base = r0 - k - 1;  // global row of local row 0
+  const int nloc = (r1 - r0) + 2 * k + 2;
+  const uint32_t kc = sbase, kf = sbase + a.W * 8;
+  const uint32_t bufs = sbase + (FORCE ? 2u : 1u) * static_cast<uint32_t>(a.W) * 8u;
+  const uint32_t bufsz = static_cast<uint32_t>(nloc) * RB;
+  const uint32_t lsm = bufs + 2u * bufsz + static_cast<uint32_t>(warp) * kResScratch;
+  const uint32_t osm = lsm + 16 * 32;
+  // Zero rows stand for the rows outside the lattice.
+  for (uint32_t o = threadIdx.x * 16u; o < 2u * bufsz; o += blockDim.x * 16u) sts128(bufs + o, 0, 0, 0, 0);
+  unsigned swaps = 0;
+  int g = a.cur;
+  for (long long done = 0; done < a.count;) {
+    const int kb = static_cast<int>(min(static_cast<long long>(k), a.count - done));
+    __syncthreads();
+    // Rows [r0 - kb, r1 + kb) of the current state into buffer 0.
+    {
+      const int lo = max(0, r0 - kb), hi = min(a.H, r1 + kb);
+      const uint32_t n16 = RB / 16u;
+      const uint32_t total = static_cast<uint32_t>(hi - lo) * n16;
+      for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+        const uint32_t rr = t / n16, c = t % n16;
+        const uint4 v = ldcg128((g ? a.g1 : a.g0) + static_cast<size_t>(lo + rr) * a.pitch + c * 16u);
+        sts128(bufs + static_cast<uint32_t>(lo + rr - base) * RB + c * 16u, v.x, v.y, v.z, v.w);
+      }
+    }
+    int sb = 0;
+    for (int j = 0; j < kb; ++j) {
+      const uint64_t s = static_cast<uint64_t>(a.first + done + j);
+      const uint64_t kcs = step_key(a.seed, kChirality, s), kfs = step_key(a.seed, kForcing, s);
+      for (int c = threadIdx.x; c < a.W; c += blockDim.x) {
+        sts64(kc + c * 8, column_key(kcs, static_cast<uint64_t>(c) + 1));
+        if (FORCE) sts64(kf + c * 8, column_key(kfs, static_cast<uint64_t>(c) + 1));
+      }
+      __syncthreads();
+      const int clo = max(0, r0 - kb + 1 + j), chi = min(a.H, r1 + kb - 1 - j);
+      const uint32_t src = bufs + static_cast<uint32_t>(sb) * bufsz;
+      const uint32_t dst = bufs + static_cast<uint32_t>(sb ^ 1) * bufsz;
+      const int units = (chi - clo) * nb;
+      for (int u = warp; u < units; u += kResWarps) {
+        const int r = clo + u / nb, b = u % nb;
+        const uint32_t off = static_cast<uint32_t>(r - base) * RB + static_cast<uint32_t>(4 + b * 32 + lane) * 4u;
+        const int pad = (b == 0 && lane < 4) ? WW * 4 : (b == nb - 1 && lane >= 28) ? -WW * 4 : 0;
+        const uint32_t y = static_cast<uint32_t>(r);
+        const bool own = r >= r0 && r < r1;
+        if (r & 1)
+          resident_row<RULE, FORCE, 1>(src + off - RB, src + off, src + off + RB, dst + off, P, pad,
+                                       kc + b * 8192, kf + b * 8192, lsm, osm, lane, y, a.k4, a.thr,
+                                       own, swaps);
+        else
+          resident_row<RULE, FORCE, 0>(src + off - RB, src + off, src + off + RB, dst + off, P, pad,
+                                       kc + b * 8192, kf + b * 8192, lsm, osm, lane, y, a.k4, a.thr,
+                                       own, swaps);
+      }
+      __syncthreads();
+      sb ^= 1;
+    }
+    // Rows [r0, r1), planes 0-6 with their pad words, into the other buffer
+    // (plane 7, the obstacles, is static in both).
+    {
+      const uint32_t n16 = 7u * P / 16u;
+      const uint32_t total = static_cast<uint32_t>(r1 - r0) * n16;
+      const uint32_t src = bufs + static_cast<uint32_t>(sb) * bufsz;
+      for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
+        const uint32_t rr = t / n16, c = t % n16;
+        const uint4 v = lds128(src + static_cast<uint32_t>(r0 + rr - base) * RB + c * 16u);
+        __stcg(reinterpret_cast<uint4*>((g ? a.g0 : a.g1) + static_cast<size_t>(r0 + rr) * a.pitch + c * 16u), v);
+      }
+    }
+    g ^= 1;
+    done += kb;
+    grid_barrier(a.bar);
+  }
+  if (FORCE) {
+    unsigned long long sw = swaps;
+    for (int o = 16; o; o >>= 1) sw += __shfl_xor_sync(0xFFFFFFFFu, sw, o);
+    if (lane == 0 && sw) atomicAdd(a.swaps, sw);
+  }
+}
+
+int resident_smem(int W, int H, int rows_per_cta, int depth, bool force) {
+  const int RB = 8 * (W / 32 + 8) * 4;
+  const int nloc = rows_per_cta + 2 * depth + 2;
+  (void)H;
+  return (force ? 2 : 1) * W * 8 + 2 * nloc * RB + kResWarps * kResScratch;
+}
+
+}  // namespace
+
+#ifndef FHPG_RESIDENT_DEPTH
+#define FHPG_RESIDENT_DEPTH 8  // cfg1 (1024^2 FHP-I): 2 -> 320, 4 -> 416, 8 -> 422, 12 -> 397 GSUPS
+#endif
+// Largest lattice (sites) the resident kernel takes: above it the streaming
+// kernels' per-launch cost is a small fraction of a step.
+#ifndef FHPG_RESIDENT_MAX_SITES
+#define FHPG_RESIDENT_MAX_SITES (4LL << 20)
+#endif
+
+int resident_plan(int W, int H, uint64_t thr, int num_sms, int* rows_per_cta, int* grid) {
+  if (W % 1024 || H < 3 || static_cast<long long>(W) * H > FHPG_RESIDENT_MAX_SITES) return 0;
+  const int rpc = (H + num_sms - 1) / num_sms;
+  const int depth = FHPG_RESIDENT_DEPTH;
+  if (resident_smem(W, H, rpc, depth, thr != 0) > 227 * 1024) return 0;
+  *rows_per_cta = rpc;
+  *grid = (H + rpc - 1) / rpc;
+  return depth;
+}
+
+// Returns the number of global-buffer flips (blocks of depth steps).
+int launch_step_resident(uint8_t* const g[2], int cur, size_t pitch, int W, int H, int rule,
+                         uint64_t seed, uint64_t thr, long long first, long long count,
+                         unsigned long long* swaps, unsigned* bar, int num_sms, cudaStream_t st,
+                         cudaError_t* err) {
+  int rpc = 0, grid = 0;
+  const int depth = resident_plan(W, H, thr, num_sms, &rpc, &grid);
+  ResArgs a{};
+  a.g0 = g[0];
+  a.g1 = g[1];
+  a.cur = cur;
+  a.pitch = pitch;
+  a.W = W;
+  a.H = H;
+  a.rows_per_cta = rpc;
+  a.depth = depth;
+  a.first = first;
+  a.count = count;
+  a.seed = seed;
+  a.thr = thr;
+  a.k4 = 4u;
+  a.swaps = swaps;
+  a.bar = bar;
+  const int smem = resident_smem(W, H, rpc, depth, thr != 0);
+  void* args[] = {&a};
+  auto go = [&](auto kernel) {
+    ensure_smem_optin(reinterpret_cast<const void*>(kernel), smem);
+    *err = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3(grid),
+                                       dim3(kResThreads), args, smem, st);
+  };
+  const bool f = thr != 0;
+  if (rule == 0) f ? go(step_resident_kernel<0, true>) : go(step_resident_kernel<0, false>);
+  else if (rule == 1) f ? go(step_resident_kernel<1, true>) : go(step_resident_kernel<1, false>);
+  else f ? go(step_resident_kernel<2, true>) : go(step_resident_kernel<2, false>);
+  return static_cast<int>((count + depth - 1) / depth);
+}
+
+}  // namespace fhpg

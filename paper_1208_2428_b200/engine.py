@@ -41,6 +41,7 @@ SIGNATURES = {
                                     C.POINTER(C.c_void_p)]),
     "fhpg_create_multi": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
                                     C.POINTER(C.c_void_p)]),
+    "fhpg_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "fhpg_strips": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                               C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "fhpg_destroy": (None, [C.c_void_p]),
@@ -203,13 +204,16 @@ class Engine:
 
     @property
     def path(self) -> str:
-        """Step kernel in use: "planes" (bit-plane circuit), "bytes" (byte
-        streaming LUT kernel) or "generic" (one thread per site)."""
+        """Step kernel in use: "planes" (bit-plane circuit: streaming kernels,
+        or for multi-step calls on small lattices the shared-memory-resident
+        kernel), "bytes" (byte streaming LUT kernel) or "generic" (one thread
+        per site)."""
         return self.PATHS[self._info()[4]]
 
     def select_path(self, path: str):
-        """"auto" (default), "bytes" (no bit-plane path) or "generic"."""
-        code = {"auto": 0, "bytes": 1, "generic": 2}[path]
+        """"auto" (default), "bytes" (no bit-plane path), "generic", or
+        "streaming" (bit planes without the resident small-lattice kernel)."""
+        code = {"auto": 0, "bytes": 1, "generic": 2, "streaming": 3}[path]
         _check(self.lib.fhpg_select_path(self.h, code))
 
     @property

@@ -1,0 +1,48 @@
+"""The shared-memory-resident kernel for small bit-plane lattices
+(fhpg_step_resident.cu): a whole multi-step advance call in one cooperative
+launch, time-blocked with deep halos (halo rows recomputed by neighbouring
+CTAs). Bit-exact against the oracle and against the streaming kernels
+(fhpg_select_path 3) on adversarial states: both row parities at CTA row
+boundaries, step counts that are not multiples of the halo depth, forcing,
+every rule with a circuit, walls and obstacles, nonzero first steps. (cfg1 itself, FHP-I 1024^2 for 1000 steps against the
+reference's digest, is tests/test_parity_gpu.py::test_cfg1_fhp1_1024, which
+now runs on this kernel.)"""
+import pytest
+
+import paper_1208_2428_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(W, H, table, mask, state, path="auto"):
+    e = P.Engine(W, H)
+    e.set_table(table)
+    if path != "auto":
+        e.select_path(path)
+    e.set_obstacles(mask)
+    e.upload(state)
+    return e
+
+
+@pytest.mark.parametrize("W,H", [(1024, 1024), (1024, 3), (1024, 37), (2048, 301), (4096, 150),
+                                 (1024, 2000)])
+@pytest.mark.parametrize("rule,fp", [("fhp3", 0.0), ("fhp3", 0.3), ("fhp1", 0.0), ("default", 0.05)])
+def test_resident_equals_oracle_and_streaming(W, H, rule, fp, port, tables):
+    state, mask = port.scramble(W, H, W + 7 * H)
+    t = tables[rule]
+    a = _engine(W, H, t, mask, state)
+    b = _engine(W, H, t, mask, state, "streaming")
+    n0 = a.step_launches
+    swa = a.advance(9, fp, 13, 11)       # 11 steps: not a multiple of the halo depth
+    assert a.step_launches - n0 == 1      # one launch for the whole call
+    swb = b.advance(9, fp, 13, 11)
+    assert swa == swb
+    out = a.download()
+    assert (out == b.download()).all()
+    if W * H <= 1 << 20:
+        ref, rsw = port.advance(state, t, 9, port.threshold(fp), 13, 11, mask=mask)
+        assert (out == ref).all()
+        assert swa == rsw
+    # a second call continues exactly (buffer parity after the flips)
+    assert a.advance(9, fp, 24, 6) == b.advance(9, fp, 24, 6)
+    assert (a.download() == b.download()).all()

@@ -8,5 +8,5 @@ mkdir -p paper_1208_2428_b200/lib/ab
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
   -Xcompiler -fPIC --expt-relaxed-constexpr -Iinclude $EXTRA -shared -o paper_1208_2428_b200/lib/ab/$name.so \
   paper_1208_2428_b200/csrc/fhpg_kernels.cu paper_1208_2428_b200/csrc/fhpg_step_fast.cu \
-  paper_1208_2428_b200/csrc/fhpg_step_planes.cu paper_1208_2428_b200/csrc/fhpg_reduce_planes.cu paper_1208_2428_b200/csrc/fhpg_capi.cu \
+  paper_1208_2428_b200/csrc/fhpg_step_planes.cu paper_1208_2428_b200/csrc/fhpg_step_resident.cu paper_1208_2428_b200/csrc/fhpg_reduce_planes.cu paper_1208_2428_b200/csrc/fhpg_capi.cu \
   paper_1208_2428_b200/csrc/fhpg_tables.cpp

@@ -18,11 +18,14 @@ except Exception:  # noqa: BLE001
     HBM_GBS = 6532.9
 
 
-def timed(W, H, table, fp, steps, seed, density, clear_rest=False, mask=None, warm=10):
+def timed(W, H, table, fp, steps, seed, density, clear_rest=False, mask=None, warm=10,
+          path="auto"):
     e = P.Engine(W, H)
     s = torch.cuda.Stream()
     e.set_stream(s.cuda_stream)
     e.set_table(P.build_table(table))
+    if path != "auto":
+        e.select_path(path)
     if mask is not None:
         e.set_obstacles(mask)
     e.init(seed, density)
@@ -34,6 +37,7 @@ def timed(W, H, table, fp, steps, seed, density, clear_rest=False, mask=None, wa
     e.advance_async(seed, thr, 0, warm)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    n0 = e.step_launches
     a.record(s)
     e.advance_async(seed, thr, warm, steps)
     b.record(s)
@@ -43,6 +47,9 @@ def timed(W, H, table, fp, steps, seed, density, clear_rest=False, mask=None, wa
     return {"W": W, "H": H, "table": table, "force_p": fp, "steps": steps,
             "obstacles": int(mask.sum()) if mask is not None else 0,
             "ms_per_step": ms / steps, "GSUPS": gsups, "path": e.path,
+            "kernel_launches": e.step_launches - n0,
+            "kernel": ("resident (one launch per call)" if e.step_launches - n0 == 1
+                       else "streaming (one launch per step)"),
             "hbm_roofline_frac": gsups * 1.875 / HBM_GBS,
             "l2_resident": 2 * (W + 256) * (H + 5) < 120e6}
 
@@ -66,6 +73,7 @@ def cylinder_mask(W, H):
 
 if __name__ == "__main__":
     out = [timed(1024, 1024, "fhp1", 0.0, 1000, 1, 0.2, clear_rest=True),
+           timed(1024, 1024, "fhp1", 0.0, 1000, 1, 0.2, clear_rest=True, path="streaming"),
            timed(4096, 2048, "fhp3", 0.01, 1000, 2, 0.2),
            timed(8192, 4096, "fhp3", 0.01, 500, 3, 0.2, mask=cylinder_mask(8192, 4096)),
            timed(16384, 16384, "fhp3", 0.0, 200, 4, 0.2),
