@@ -195,6 +195,13 @@ int fhpg_force_generic(fhpg_engine* e, int on);
  * are identical on every path. */
 int fhpg_select_path(fhpg_engine* e, int path);
 
+/* Introspection: the halo depth (steps per block, > 0) the shared-memory-
+ * resident kernel would run a multi-step fhpg_advance call with at this
+ * forcing threshold, or 0 when the call goes to the streaming kernels (the
+ * lattice or its shared-memory footprint is too large, a strip engine, or a
+ * path other than automatic selected). */
+int fhpg_resident_depth(fhpg_engine* e, uint64_t force_thr, int* depth);
+
 #ifdef __cplusplus
 }
 #endif

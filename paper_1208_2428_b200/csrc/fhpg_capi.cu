@@ -1075,4 +1075,16 @@ int fhpg_select_path(fhpg_engine* e, int path) {
   });
 }
 
+int fhpg_resident_depth(fhpg_engine* e, uint64_t thr, int* depth) {
+  return guarded([&] {
+    need(e);
+    if (!depth) invalid("depth is null");
+    int rpc = 0, grid = 0;
+    *depth = (!e->multi() && e->planes && e->path_pref == 0 && e->row_begin == 0 &&
+              e->row_end == e->H)
+                 ? resident_plan(e->W, e->H, thr, e->num_sms, &rpc, &grid)
+                 : 0;
+  });
+}
+
 }  // extern "C"

@@ -13,21 +13,14 @@
 //             bit is left unchanged.
 //  * FHP-III — collision-saturated with rest particle: every fluid state whose
 //             (mass, momentum) class has another member moves to another
-//             member. Zero-momentum classes rotate by +60 (chirality 1) or
-//             -60 degrees (chirality 0); classes of nonzero momentum p are
-//             ordered in the frame that rotates p into a fixed 60-degree
-//             sector, two-member classes swap, larger ones cycle forward
-//             (chirality 0) or backward (chirality 1). The rule commutes with
-//             lattice rotations, and a mirror maps the chirality-0 rule onto
-//             the chirality-1 rule.
+//             member, by the bit-sliced circuit of fhpg_fhp3_logic.cuh (the
+//             table is that circuit evaluated per state). The rule commutes
+//             with lattice rotations, and a mirror maps the chirality-0 rule
+//             onto the chirality-1 rule.
 //
 // All variants use the reference's obstacle rule: full bounce-back keeping
 // the rest and obstacle bits (collision.cpp:62-66).
-#include <algorithm>
-#include <array>
 #include <cstdint>
-#include <map>
-#include <vector>
 
 #include "../../include/fhpg_tables.h"
 #include "fhpg_fhp3_logic.cuh"
@@ -55,19 +48,6 @@ void momentum(unsigned s, int& px, int& py) {
       px += kPx[k];
       py += kPy[k];
     }
-}
-
-// Rotation k (in mover bits; +1 bit turns every vector by -60 degrees) that
-// maps the momentum of state s into the canonical sector [0, 60) degrees.
-// Exact integer test in the reference's (px, py) units, where physical
-// (x, y) = (px/2, py*sqrt(3)/2): angle in [0, 60) <=> py >= 0 and py < px.
-int sector(unsigned s) {
-  for (int k = 0; k < 6; ++k) {
-    int px, py;
-    momentum(rot(s, k), px, py);
-    if (py >= 0 && py < px) return k;
-  }
-  return 0;  // zero momentum
 }
 
 uint8_t bounce(unsigned s) { return static_cast<uint8_t>((s & 0xC0u) | reverse6(s & 0x3Fu)); }
@@ -102,54 +82,6 @@ void build_fhp3(uint8_t* t) {
       out |= (orr & 1u) << 6;
       t[(ch << 8) | s] = static_cast<uint8_t>(out);
     }
-}
-
-// The class-cycle construction used before the rule was written as logic
-// (kept for reference; not used).
-[[maybe_unused]] void build_fhp3_class_cycles(uint8_t* t) {
-  // Group fluid states by (mass, px, py).
-  std::map<std::array<int, 3>, std::vector<unsigned>> classes;
-  for (unsigned s = 0; s < 128; ++s) {
-    int px, py;
-    momentum(s, px, py);
-    classes[{popc7(s), px, py}].push_back(s);
-  }
-  std::array<std::array<uint8_t, 128>, 2> out{};
-  for (auto& [key, members] : classes) {
-    const int px = key[1], py = key[2];
-    const size_t n = members.size();
-    if (n == 1) {
-      out[0][members[0]] = out[1][members[0]] = static_cast<uint8_t>(members[0]);
-      continue;
-    }
-    if (px == 0 && py == 0) {
-      bool ok = true;
-      for (unsigned s : members)
-        if (rot(s, 1) == s) ok = false;
-      if (ok) {
-        for (unsigned s : members) {
-          out[1][s] = static_cast<uint8_t>(rot(s, 1));
-          out[0][s] = static_cast<uint8_t>(rot(s, -1));
-        }
-        continue;
-      }
-    }
-    // Canonical frame: rotate so that p lies in the fixed sector, order the
-    // members there by byte value, cycle.
-    const int k = (px == 0 && py == 0) ? 0 : sector(members[0]);
-    std::vector<std::pair<unsigned, unsigned>> canon;  // (canonical, original)
-    for (unsigned s : members) canon.push_back({rot(s, k), s});
-    std::sort(canon.begin(), canon.end());
-    for (size_t i = 0; i < n; ++i) {
-      const unsigned up = canon[(i + 1) % n].second;
-      const unsigned down = canon[(i + n - 1) % n].second;
-      out[0][canon[i].second] = static_cast<uint8_t>(up);
-      out[1][canon[i].second] = static_cast<uint8_t>(down);
-    }
-  }
-  for (int ch = 0; ch < 2; ++ch)
-    for (unsigned s = 0; s < 256; ++s)
-      t[(ch << 8) | s] = (s & 0x80u) ? bounce(s) : out[ch][s];
 }
 
 // collision.cpp:22-51 (the reference's DEFAULT rules), restated.

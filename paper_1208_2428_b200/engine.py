@@ -69,6 +69,7 @@ SIGNATURES = {
                             C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), u64p]),
     "fhpg_force_generic": (C.c_int, [C.c_void_p, C.c_int]),
     "fhpg_select_path": (C.c_int, [C.c_void_p, C.c_int]),
+    "fhpg_resident_depth": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int)]),
     # include/fhpg_tables.h
     "fhpg_build_table": (C.c_int, [C.c_int, u8p]),
     "fhpg_validate_table": (C.c_int, [u8p, C.POINTER(C.c_int)]),
@@ -215,6 +216,13 @@ class Engine:
         "streaming" (bit planes without the resident small-lattice kernel)."""
         code = {"auto": 0, "bytes": 1, "generic": 2, "streaming": 3}[path]
         _check(self.lib.fhpg_select_path(self.h, code))
+
+    def resident_depth(self, force_p: float = 0.0) -> int:
+        """Halo depth of the shared-memory-resident kernel for a multi-step
+        advance at this forcing probability (0: the streaming kernels run)."""
+        d = C.c_int(0)
+        _check(self.lib.fhpg_resident_depth(self.h, bernoulli_threshold(force_p), C.byref(d)))
+        return d.value
 
     @property
     def step_launches(self) -> int:
