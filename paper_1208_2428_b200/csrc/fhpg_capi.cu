@@ -1082,7 +1082,7 @@ int fhpg_resident_depth(fhpg_engine* e, uint64_t thr, int* depth) {
     int rpc = 0, grid = 0;
     *depth = (!e->multi() && e->planes && e->path_pref == 0 && e->row_begin == 0 &&
               e->row_end == e->H)
-                 ? resident_plan(e->W, e->H, thr, e->num_sms, &rpc, &grid)
+                 ? fhpg::resident_plan(e->W, e->H, thr, e->num_sms, &rpc, &grid)
                  : 0;
   });
 }
