@@ -174,8 +174,10 @@ void create(int W, int H, int rb, int re, int device, fhpg_engine** out) {
     e->row_end = re;
     e->nrows = re - rb;
     e->device = device;
-    // Room for the bit-plane rows (W + 256 bytes) when the width allows them.
-    e->pitch = (static_cast<size_t>(W) + 15) / 16 * 16 + (fhpg::planes_ok(W) ? 256 : 0);
+    // Room for the bit-plane rows (W + 2048 bytes, line-aligned) when the
+    // width allows them.
+    e->pitch = fhpg::planes_ok(W) ? fhpg::planes_row_bytes(W)
+                                  : (static_cast<size_t>(W) + 15) / 16 * 16;
     // halo above, rows, halo below, 3 spare zero rows the streaming kernels may prefetch
     const size_t bytes = (static_cast<size_t>(e->nrows) + 5) * e->pitch;
     for (int i = 0; i < 2; ++i) {

@@ -59,17 +59,36 @@ int launch_step_fast(const StepArgs& a, int num_sms, cudaStream_t st);
 bool fast_path_ok(int W);
 
 // Bit-plane path (fhpg_step_planes.cu): rows hold 8 planes (plane p: bit p
-// of every node; bit j of word i = column 32 i + j), each W/32 words plus 4
-// periodic-wrap pad words on either side: planes_row_bytes(W) = W + 256.
+// of every node; bit j of word i = column 32 i + j). A plane row is
+// plane_stride_words(W) = W/32 + 64 words: 32 lead words, the W/32 data
+// words, 32 trail words. The data starts on a 128-byte line (W % 1024 == 0,
+// row pitch planes_row_bytes(W) = W + 2048), so the step kernel's band
+// stores are whole lines and never share a sector with another band's. The
+// lead words [24, 32) hold the periodic wrap of data words W/32-8 .. W/32-1
+// and the trail words [W/32+32, W/32+40) that of data words 0..7 — one
+// 32-byte sector each (readers use the inner 4 words).
+constexpr int kPlaneLead = 32;
+constexpr int kPlaneWrap = 8;
+#ifndef FHPG_PLANE_TRAIL
+#define FHPG_PLANE_TRAIL 32
+#endif
+constexpr int kPlaneTrail = FHPG_PLANE_TRAIL;
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+constexpr int plane_stride_words(int W) { return W / 32 + kPlaneLead + kPlaneTrail; }
 bool planes_ok(int W);  // W % 1024 == 0
 int planes_words_per_lane(int W);
 size_t planes_row_bytes(int W);
 // TMA descriptors (CUtensorMap, 64-byte aligned, 128 bytes each) of a plane
-// buffer whose row 0 is at `buffer` (the top halo row), `rows` rows: kind 0
-// = row loads (band + edge words, 8 planes), 1 = band stores (7 planes), 2 =
-// pad stores (4 words, 7 planes), 3 = FHPG_BOX_ROWS-row loads, 4 / 5 = 2-row
-// band / pad stores.
-constexpr int kPlaneMaps = 6;
+// buffer whose row 0 is at `buffer` (the top halo row), `rows` rows:
+// kMapLoad = row loads (band + 4 edge words on either side, 8 planes),
+// kMapStore = band stores (7 planes), kMapLoadRows = FHPG_BOX_ROWS-row loads,
+// kMapPad = periodic-wrap sector stores (kPlaneWrap words, 7 planes; the
+// per-warp kernel), kMapSide = 4 words x 8 planes x FHPG_BOX_ROWS rows (the
+// ring kernel's edge bands load the wrap words instead of storing sectors).
+constexpr int kMapLoad = 0, kMapStore = 1, kMapLoadRows = 2, kMapPad = 3, kMapSide = 4;
+constexpr int kPlaneMaps = 5;
 bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows, int kind);
 // One time step with a collision circuit (a.rule) over rows [row_lo, row_hi)
 // (and the optional second range): loads through the source buffer's maps,

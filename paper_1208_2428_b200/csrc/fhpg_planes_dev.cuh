@@ -192,14 +192,16 @@ struct Geo {
   static constexpr int kSlot = 8 * kPlane;
   static constexpr int kSlots = FHPG_PLANES_SLOTS;
   // Output staging (7 planes x band words, the TMA store source) followed by
-  // the two pad boxes (7 x 4 words each). The walk's list and result words
-  // reuse the staging area: they are dead before the row's outputs land.
+  // the edge bands' wrap-sector box (7 planes x kPlaneWrap words). The
+  // walk's list and result words reuse the staging area: they are dead
+  // before the row's outputs land.
   static constexpr int kStage = 7 * 4 * kBandWords;
-  static constexpr int kPadL = kStage, kPadR = kStage + 128;  // TMA sources: 128 B aligned
+  static constexpr int kPad = kStage;             // TMA source: 128 B aligned
   static constexpr int kList = 16 * kBandWords;   // walk list entries (uint4), inside the stage
   static constexpr int kOut = 4 * kBandWords;     // walk result words, after the list
-  static_assert(kList + kOut <= kStage + 240, "walk scratch must fit the staging area");
+  static_assert(kList + kOut <= kStage, "walk scratch must fit the staging area");
   static_assert(kStage % 128 == 0, "TMA store sources are 128 B aligned");
+  static_assert(7 * 4 * kPlaneWrap <= 256, "wrap box");
   static constexpr int kStageAll = kStage + 256;
   static constexpr int kWarp = (kSlots * kSlot + kStageAll + 8 * kSlots + 127) / 128 * 128;
   static constexpr uint32_t kRowBytes = kSlot;
@@ -208,11 +210,10 @@ struct Geo {
 struct Lanes {
   int lane;
   int WW;           // words per plane row (W / 32)
-  int PW;           // words per padded plane row (W / 32 + 8)
+  int PW;           // words per plane row (plane_stride_words)
   int w0;           // first word of the band
-  int pad;          // this lane's words also go to this pad staging offset (-1: none)
-  int padx;         // bit 0: left pad box, bit 1: right pad box (word WW + 4 = (padx >> 2) + 4)
-  bool pad_band;    // warp-uniform: some lane of the band writes a pad
+  int padx;         // bit 0: last band (left wrap sector), bit 1: first band (right wrap
+                    // sector), padx >> 2 = WW
 };
 
 // Plane words of this lane from a slot: aligned, or shifted by one column.
@@ -248,6 +249,35 @@ __device__ __forceinline__ void rd_shr(uint32_t a, uint32_t (&o)[NW]) {
   uint32_t v[NW];
   rd_al<NW>(a, v);
   const uint32_t next = lds32(a + 4 * NW);
+#pragma unroll
+  for (int i = 0; i < NW - 1; ++i) o[i] = __funnelshift_r(v[i], v[i + 1], 1);
+  o[NW - 1] = __funnelshift_r(v[NW - 1], next, 1);
+}
+
+// The same reads for the lanes at a lattice edge (E: 0 = interior band;
+// 1 = band 0 of several, lane 0's previous word is the periodic wrap, read
+// from the side buffer at `wp`; 2 = the last band of several, lane 31's
+// next word, from `wp`; 3 = a single band, both wraps inside the slot).
+template <int NW, int E>
+__device__ __forceinline__ void rd_shl_e(uint32_t a, uint32_t wp, int lane, uint32_t (&o)[NW]) {
+  uint32_t v[NW];
+  rd_al<NW>(a, v);
+  uint32_t pa = a - 4;
+  if constexpr (E == 1) pa = lane == 0 ? wp : pa;
+  if constexpr (E == 3) pa = lane == 0 ? a + (32 * NW - 1) * 4 : pa;
+  const uint32_t prev = lds32(pa);
+  o[0] = __funnelshift_l(prev, v[0], 1);
+#pragma unroll
+  for (int i = 1; i < NW; ++i) o[i] = __funnelshift_l(v[i - 1], v[i], 1);
+}
+template <int NW, int E>
+__device__ __forceinline__ void rd_shr_e(uint32_t a, uint32_t wp, int lane, uint32_t (&o)[NW]) {
+  uint32_t v[NW];
+  rd_al<NW>(a, v);
+  uint32_t na = a + 4 * NW;
+  if constexpr (E == 2) na = lane == 31 ? wp : na;
+  if constexpr (E == 3) na = lane == 31 ? a - 31 * NW * 4 : na;
+  const uint32_t next = lds32(na);
 #pragma unroll
   for (int i = 0; i < NW - 1; ++i) o[i] = __funnelshift_r(v[i], v[i + 1], 1);
   o[NW - 1] = __funnelshift_r(v[NW - 1], next, 1);

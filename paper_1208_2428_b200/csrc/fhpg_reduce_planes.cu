@@ -43,7 +43,7 @@ __device__ __forceinline__ void load_word(const uint8_t* base, size_t pitch, int
                                           int i, uint32_t (&w)[8]) {
   const uint32_t* row = reinterpret_cast<const uint32_t*>(base + r * static_cast<long long>(pitch));
 #pragma unroll
-  for (int p = 0; p < 8; ++p) w[p] = __ldcs(row + p * PW + 4 + i);
+  for (int p = 0; p < 8; ++p) w[p] = __ldcs(row + p * PW + kPlaneLead + i);
 }
 
 template <typename T>
@@ -54,7 +54,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 __global__ void reduce_global_planes_kernel(const uint8_t* base, size_t pitch, int W, int nrows,
                                             long long* acc) {
-  const int WW = W >> 5, PW = WW + 8;
+  const int WW = W >> 5, PW = plane_stride_words(W);
   const long long n = static_cast<long long>(nrows) * WW;
   long long mass = 0, px = 0, py = 0;
   for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < n;
@@ -92,7 +92,7 @@ __global__ void reduce_rows_planes_kernel(const uint8_t* base, size_t pitch, int
   const int r = blockIdx.x;
   const long long gr = row0 + r;
   if (gr < 1 || gr > H - 2) return;
-  const int WW = W >> 5, PW = WW + 8;
+  const int WW = W >> 5, PW = plane_stride_words(W);
   long long px = 0;
   int fluid = 0;
   for (int i = threadIdx.x; i < WW; i += blockDim.x) {
@@ -130,7 +130,7 @@ __global__ void reduce_cells_planes_kernel(const uint8_t* base, size_t pitch, in
                                            long long row0, long long H, int B, int cells_x,
                                            int cy0, int ncy, int* nodes, int* particles,
                                            long long* pxo, long long* pyo) {
-  const int WW = W >> 5, PW = WW + 8;
+  const int WW = W >> 5, PW = plane_stride_words(W);
   const long long n = static_cast<long long>(ncy) * WW;
   for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<long long>(gridDim.x) * blockDim.x) {

@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int WW = a.W >> 5;
-  const uint32_t P = static_cast<uint32_t>(WW + 8) * 4u;  // plane row (pads included)
+  const uint32_t P = static_cast<uint32_t>(WW + 8) * 4u;  // shared plane row (4 wrap words each side)
+  const uint32_t GP = static_cast<uint32_t>(plane_stride_words(a.W)) * 4u;  // global plane row
   const uint32_t RB = 8u * P;                              // row of 8 planes
   const int nb = a.W >> 10;                                // 1024-column bands
   const int k = a.depth;
@@ -161,13 +162,19 @@ __global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a
     const int kb = static_cast<int>(min(static_cast<long long>(k), a.count - done));
     __syncthreads();
     // Rows [r0 - kb, r1 + kb) of the current state into buffer 0.
+    // (Shared memory keeps 4 wrap words on either side of each plane's data,
+    // made here from the data words: the streaming ring kernel does not
+    // maintain the global rows' wrap sectors.)
     {
       const int lo = max(0, r0 - kb), hi = min(a.H, r1 + kb);
-      const uint32_t n16 = RB / 16u;
+      const uint32_t n16 = RB / 16u, p16 = P / 16u;
       const uint32_t total = static_cast<uint32_t>(hi - lo) * n16;
       for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
-        const uint32_t rr = t / n16, c = t % n16;
-        const uint4 v = ldcg128((g ? a.g1 : a.g0) + static_cast<size_t>(lo + rr) * a.pitch + c * 16u);
+        const uint32_t rr = t / n16, c = t % n16, pl = c / p16, j = c % p16;
+        const int d = static_cast<int>(4 * j) - 4;  // data word of the chunk
+        const uint32_t gw = kPlaneLead + static_cast<uint32_t>((d + WW) % WW);
+        const uint4 v = ldcg128((g ? a.g1 : a.g0) + static_cast<size_t>(lo + rr) * a.pitch +
+                                pl * GP + gw * 4u);
         sts128(bufs + static_cast<uint32_t>(lo + rr - base) * RB + c * 16u, v.x, v.y, v.z, v.w);
       }
     }
@@ -202,16 +209,21 @@ __global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a
       __syncthreads();
       sb ^= 1;
     }
-    // Rows [r0, r1), planes 0-6 with their pad words, into the other buffer
-    // (plane 7, the obstacles, is static in both).
+    // Rows [r0, r1), planes 0-6 with their wrap sectors (global words
+    // kPlaneLead - 8 .. kPlaneLead + WW + 8), into the other buffer (plane
+    // 7, the obstacles, is static in both).
     {
-      const uint32_t n16 = 7u * P / 16u;
+      const uint32_t p16 = static_cast<uint32_t>(WW + 2 * kPlaneWrap) / 4u, n16 = 7u * p16;
       const uint32_t total = static_cast<uint32_t>(r1 - r0) * n16;
       const uint32_t src = bufs + static_cast<uint32_t>(sb) * bufsz;
       for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
-        const uint32_t rr = t / n16, c = t % n16;
-        const uint4 v = lds128(src + static_cast<uint32_t>(r0 + rr - base) * RB + c * 16u);
-        __stcg(reinterpret_cast<uint4*>((g ? a.g0 : a.g1) + static_cast<size_t>(r0 + rr) * a.pitch + c * 16u), v);
+        const uint32_t rr = t / n16, c = t % n16, pl = c / p16, j = c % p16;
+        const int d = static_cast<int>(4 * j) - kPlaneWrap;  // data word of the chunk
+        const uint32_t sw = 4u + static_cast<uint32_t>((d + WW) % WW);
+        const uint4 v = lds128(src + static_cast<uint32_t>(r0 + rr - base) * RB + pl * P + sw * 4u);
+        __stcg(reinterpret_cast<uint4*>((g ? a.g0 : a.g1) + static_cast<size_t>(r0 + rr) * a.pitch +
+                                        pl * GP + (kPlaneLead - kPlaneWrap + 4 * j) * 4u),
+               v);
       }
     }
     g ^= 1;

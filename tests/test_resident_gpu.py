@@ -51,3 +51,26 @@ def test_resident_equals_oracle_and_streaming(W, H, rule, fp, port, tables):
     # a second call continues exactly (buffer parity after the flips)
     assert a.advance(9, fp, 24, 6) == b.advance(9, fp, 24, 6)
     assert (a.download() == b.download()).all()
+
+
+@pytest.mark.parametrize("W,H", [(2048, 301), (4096, 150), (1024, 1024)])
+def test_mixed_single_and_multi_step_calls(W, H, port, tables):
+    """Single-step calls run the streaming kernels (the ring kernel keeps no
+    periodic-wrap sectors in the plane rows), multi-step calls the resident
+    kernel (which rebuilds the wrap words from the data): any interleaving
+    equals the oracle."""
+    state, mask = port.scramble(W, H, 3 * W + H)
+    t = tables["fhp3"]
+    a = _engine(W, H, t, mask, state)
+    step, sw = 40, 0
+    for n in (1, 5, 1, 1, 7, 1):
+        sw += a.advance(2, 0.0, step, n)
+        step += n
+    if W * H <= 1 << 20:
+        ref, rsw = port.advance(state, t, 2, 0, 40, step - 40, mask=mask)
+        assert (a.download() == ref).all()
+        assert sw == rsw
+    else:
+        b = _engine(W, H, t, mask, state, "streaming")
+        b.advance(2, 0.0, 40, step - 40)
+        assert (a.download() == b.download()).all()

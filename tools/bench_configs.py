@@ -51,7 +51,7 @@ def timed(W, H, table, fp, steps, seed, density, clear_rest=False, mask=None, wa
             "kernel": ("resident (one launch per call)" if e.step_launches - n0 == 1
                        else "streaming (one launch per step)"),
             "hbm_roofline_frac": gsups * 1.875 / HBM_GBS,
-            "l2_resident": 2 * (W + 256) * (H + 5) < 120e6}
+            "l2_resident": 2 * (W + 2048) * (H + 5) < 120e6}
 
 
 def cylinder_mask(W, H):
