@@ -386,6 +386,9 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 #ifndef FHPG_EXTRA_BUBBLE_ROWS
 #define FHPG_EXTRA_BUBBLE_ROWS 20
 #endif
+#ifndef FHPG_RING_TAGS
+#define FHPG_RING_TAGS 0  // 1: consumers poll per-slot tags before the parity wait
+#endif
 #ifndef FHPG_RING_CONS
 #define FHPG_RING_CONS 31
 #endif
@@ -421,6 +424,15 @@ struct RingGeo {
   static constexpr int kBox = FHPG_BOX_ROWS;     // source rows per TMA box (a "group")
   static constexpr int kGroups = kRing / kBox;   // ring slots of whole groups
   static_assert(kRing % kBox == 0, "row groups");
+  // Full barriers, one per group modulo 4 kGroups. A consumer waiting on
+  // group P has finished its previous row (31 rows = at most 9 groups back),
+  // so the producer has issued group P - 9 and with it every group up to
+  // P - 9 - kGroups has been consumed: the barrier's use for group
+  // P - 4 kGroups is complete and the parity wait for group P is unambiguous
+  // (no slot tags). Needs the static row assignment (FHPG_DYN_ROWS 0).
+  static constexpr int kFullBars = 4 * kGroups;
+  static_assert(kFullBars <= kRing, "full barriers fit the per-slot allocation");
+  static_assert(FHPG_RING_TAGS || (kCons <= 31 && !FHPG_DYN_ROWS), "tag-free ring bound");
   // Side buffer of the edge bands: per group, the 4 data words across the
   // periodic wrap of every plane and row ([kBox rows][8 planes][4 words]).
   static constexpr int kSideGroup = kBox * 8 * 16;
@@ -546,28 +558,33 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
           mbar_wait(empty + k * 8, (P / kG - 1) & 1u);
 #endif
         }
+#if FHPG_RING_TAGS
         {  // tag: an atomic store (consumers poll it; not a data race)
           uint32_t prev;
           asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(prev) : "r"(tags + k * 4), "r"(P) : "memory");
         }
+        const uint32_t fb = full + k * 8;
+#else
+        const uint32_t fb = full + (P % RG::kFullBars) * 8;
+#endif
         const bool inA = P < gA;
         const int word = (inA ? bA : bA + 1) * G::kBandWords + kPlaneLead - 4;  // band - 4 words
         const int trow = inA ? RA0 + static_cast<int>(B * P) : row_lo + static_cast<int>(B * P - offB);
 #if FHPG_STREAM_ONLY == 3 || FHPG_STREAM_ONLY >= 5  // timing experiments: no loads
         if (FHPG_STREAM_ONLY >= 5 && P < kG) {  // 5, 6: compute on the first ring fill
-          mbar_expect_tx(full + k * 8, B * G::kRowBytes);
-          tma_row(ring + B * k * G::kSlot, &map2, word, trow, full + k * 8);
+          mbar_expect_tx(fb, B * G::kRowBytes);
+          tma_row(ring + B * k * G::kSlot, &map2, word, trow, fb);
         } else {
-          mbar_arrive(full + k * 8, 1);
+          mbar_arrive(fb, 1);
         }
 #else
         const int e = edge_of(inA ? bA : bA + 1);
         const bool sided = e == 1 || e == 2;
-        mbar_expect_tx(full + k * 8, B * G::kRowBytes + (sided ? RG::kSideGroup : 0));
-        tma_row(ring + B * k * G::kSlot, &map2, word, trow, full + k * 8);  // tensor rows
+        mbar_expect_tx(fb, B * G::kRowBytes + (sided ? RG::kSideGroup : 0));
+        tma_row(ring + B * k * G::kSlot, &map2, word, trow, fb);  // tensor rows
         if (sided)  // data words W/32-4 .. W/32-1 (left wrap) or 0 .. 3 (right wrap)
           tma_row(side + k * RG::kSideGroup, &sidemap,
-                  e == 1 ? kPlaneLead + (a.W >> 5) - 4 : kPlaneLead, trow, full + k * 8);
+                  e == 1 ? kPlaneLead + (a.W >> 5) - 4 : kPlaneLead, trow, fb);
 #endif
         // Ring indices no destination row reads (the tail of part A's last
         // group when part B follows) still count 3 arrivals each, or the
@@ -624,6 +641,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
       for (uint32_t d = 0; d < 3; ++d) {
         const uint32_t P = (i + d) / B;
         if (d == 0 || ((i + d) % B) == 0) {  // a new group
+#if FHPG_RING_TAGS
           const uint32_t kp = P % kG;
           for (;;) {
             uint32_t tag;
@@ -633,6 +651,9 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
             __nanosleep(FHPG_TAG_SLEEP);
           }
           mbar_wait(full + kp * 8, (P / kG) & 1u);
+#else
+          mbar_wait(full + (P % RG::kFullBars) * 8, (P / RG::kFullBars) & 1u);
+#endif
         }
         sl[d] = ring + ((i + d) % RG::kRing) * G::kSlot + lane_off;
       }
