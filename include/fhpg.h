@@ -186,6 +186,13 @@ int fhpg_info(fhpg_engine* e, int* width, int* height, int* row_begin, int* row_
 /* Testing aid: force the generic (one-thread-per-site) step kernel. */
 int fhpg_force_generic(fhpg_engine* e, int on);
 
+/* Testing aid: rows per column-key base of the bit-plane kernels (the
+ * kernels fold each band's column keys at a base row and re-key — or, in
+ * the per-warp kernel, hash from the step keys — where a key's low word
+ * would leave its 2^30 block; this caps that span, 0xFFFFFFFF = automatic).
+ * Results are identical for every value. */
+int fhpg_debug_key_span(fhpg_engine* e, uint32_t rows);
+
 /* Step-kernel selection: 0 = automatic (bit-plane path when the table has a
  * bit-sliced circuit — FHP-III, FHP-I, DEFAULT — and W % 1024 == 0, with the
  * shared-memory-resident kernel for multi-step calls on small lattices; else

@@ -29,6 +29,7 @@ struct fhpg_engine {
   bool table_planes = false;
   int planes_rule = 2;                   // circuit of the table: FHPG_RULES_* (fhpg_tables.h)
   int path_pref = 0;                     // 0 auto, 1 byte fast path, 2 generic, 3 streaming planes
+  uint32_t span_cap = 0xFFFFFFFFu;       // fhpg_debug_key_span (testing aid)
   uint8_t* scratch = nullptr;            // nrows * pitch
   alignas(64) unsigned char tmap[2][fhpg::kPlaneMaps][128];  // TMA descriptors of buf[0], buf[1] (planes)
   bool scratch_valid = false;
@@ -329,6 +330,7 @@ void step_loop(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t first, int64
     a.thr = thr;
     a.swaps = e->swaps;
     a.rule = e->planes_rule;
+  a.span_cap = e->span_cap;
     if (i + 1 < count) {
       a.zc_next = e->keys((s + 1) & 1, 0);
       a.zf_next = force ? e->keys((s + 1) & 1, 1) : nullptr;
@@ -385,6 +387,7 @@ void step_part(fhpg_engine* e, uint64_t seed, uint64_t thr, int64_t step, int pa
   a.thr = thr;
   a.swaps = e->swaps;
   a.rule = e->planes_rule;
+  a.span_cap = e->span_cap;
   const bool interior = e->nrows >= 3;
   auto run = [&](int lo, int hi, bool with_next_keys) {
     StepArgs b = a;
@@ -1062,6 +1065,13 @@ int fhpg_force_generic(fhpg_engine* e, int on) {
       p->path_pref = on ? 2 : 0;
       sync_layout(p);
     });
+  });
+}
+
+int fhpg_debug_key_span(fhpg_engine* e, uint32_t rows) {
+  return guarded([&] {
+    need(e);
+    each(e, [&](fhpg_engine* p) { p->span_cap = rows; });
   });
 }
 

@@ -85,6 +85,60 @@ FHPG_HD uint32_t chir_bit(uint64_t z, uint32_t four) {
   const uint32_t lo2 = z1lo ^ ((z1lo >> 27) | (z1hi << 5));
   return (lo2 * kC2s) >> 31;
 }
+// The same bit as a mask: 0 or ~0u (arithmetic shift of the sign).
+FHPG_HD uint32_t chir_mask(uint64_t z, uint32_t four) {
+  const uint32_t lo = static_cast<uint32_t>(z), hi = static_cast<uint32_t>(z >> 32);
+  const uint32_t zl = lo ^ (lo >> 30) ^ (hi * four);
+  const uint32_t g = (hi ^ (hi >> 30)) * static_cast<uint32_t>(kC1);
+  const uint64_t w = static_cast<uint64_t>(zl) * static_cast<uint32_t>(kC1) +
+                     (static_cast<uint64_t>(g) << 32);
+  const uint32_t z1lo = static_cast<uint32_t>(w);
+  const uint32_t z1hi = static_cast<uint32_t>(w >> 32) + zl * static_cast<uint32_t>(kC1 >> 32);
+  const uint32_t lo2 = z1lo ^ ((z1lo >> 27) | (z1hi << 5));
+  return static_cast<uint32_t>(static_cast<int32_t>(lo2 * kC2s) >> 31);
+}
+
+// Column terms precomputed per (column, key base row b): with K = column key
+// + b, lo/hi its words, a site at row b + dy has z = K + dy. While lo + dy
+// stays inside the same 2^30-aligned block as lo (no carry into the high
+// word, same lo >> 30), the hash inputs that depend on the column alone fold
+// into two words:
+//   t2 = (hi << 2) ^ (lo >> 30)          so lo32(z ^ z >> 30) = (lo + dy) ^ t2
+//   g  = lo32((hi ^ hi >> 30) * C1)      the high word's share of z1's high word
+// (dy < colkey_span(lo) guarantees it; other rows take the full hash).
+struct ColKey {
+  uint32_t lo, t2, g;
+};
+FHPG_HD ColKey col_key_terms(uint64_t K) {
+  const uint32_t lo = static_cast<uint32_t>(K), hi = static_cast<uint32_t>(K >> 32);
+  return {lo, (hi << 2) ^ (lo >> 30), (hi ^ (hi >> 30)) * static_cast<uint32_t>(kC1)};
+}
+// Rows dy in [0, span) keep lo + dy inside lo's 2^30-aligned block.
+FHPG_HD uint32_t colkey_span(uint32_t lo) { return (1u << 30) - (lo & ((1u << 30) - 1u)); }
+// z1 = (z ^ z >> 30) * C1 from the folded terms: (low word, high word).
+FHPG_HD void colkey_z1(uint32_t l, uint32_t t2, uint32_t g, uint32_t& z1lo, uint32_t& z1hi) {
+  const uint32_t zl = l ^ t2;
+  const uint64_t w = static_cast<uint64_t>(zl) * static_cast<uint32_t>(kC1);
+  z1lo = static_cast<uint32_t>(w);
+  z1hi = static_cast<uint32_t>(w >> 32) + zl * static_cast<uint32_t>(kC1 >> 32) + g;
+}
+// Chirality mask (0 or ~0u) of the site at dy: bit 0 of fin64(K + dy).
+FHPG_HD uint32_t chir_mask_pre(uint32_t l, uint32_t t2, uint32_t g) {
+  uint32_t z1lo, z1hi;
+  colkey_z1(l, t2, g, z1lo, z1hi);
+  const uint32_t lo2 = z1lo ^ ((z1lo >> 27) | (z1hi << 5));
+  return static_cast<uint32_t>(static_cast<int32_t>(lo2 * kC2s) >> 31);
+}
+// High word of fin64(K + dy) (the forcing draw, rng.hpp:37-42).
+FHPG_HD uint32_t fin64_hi_pre(uint32_t l, uint32_t t2, uint32_t g) {
+  uint32_t z1lo, z1hi;
+  colkey_z1(l, t2, g, z1lo, z1hi);
+  const uint32_t ulo = z1lo ^ ((z1lo >> 27) | (z1hi << 5));
+  const uint32_t uhi = z1hi ^ (z1hi >> 27);
+  const uint32_t z2hi = static_cast<uint32_t>((static_cast<uint64_t>(ulo) * static_cast<uint32_t>(kC2)) >> 32) +
+                        ulo * static_cast<uint32_t>(kC2 >> 32) + uhi * static_cast<uint32_t>(kC2);
+  return z2hi ^ (z2hi >> 31);
+}
 
 // rng.hpp:37-42: bernoulli(word, p) == (word >> 32) < threshold(p).
 inline uint64_t bernoulli_threshold(double p) {

@@ -43,6 +43,7 @@ struct StepArgs {
   int segs1 = 0;             // row segments of the first range (bit-plane ring kernel)
   int segs2 = 0;             //   ... of the second range
   int extra_rows = 0;        // ring kernel: last rows of every band done by the extra CTAs
+  uint32_t span_cap = 0xFFFFFFFFu;  // bit-plane kernels: rows per column-key base (testing aid)
   int rule = 2;              // bit-plane kernels: collision circuit, 2 = FHP-III, 1 = FHP-I,
                              // 0 = DEFAULT (FHPG_RULES_*)
 };

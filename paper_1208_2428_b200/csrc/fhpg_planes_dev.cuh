@@ -121,12 +121,23 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
 }
+// Suspend-time hint (ns) of the ring waits: a waiting warp sleeps in the
+// barrier until the phase completes instead of re-polling (0: no hint).
+#ifndef FHPG_WAIT_HINT
+#define FHPG_WAIT_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done;
   do {
+#if FHPG_WAIT_HINT
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done) : "r"(bar), "r"(parity), "n"(FHPG_WAIT_HINT) : "memory");
+#else
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+#endif
   } while (!done);
 }
 // One TMA box {72 words, 8 planes, 1 row} of the plane tensor.
@@ -181,14 +192,18 @@ __device__ __forceinline__ void stv(uint32_t* p, const uint32_t (&v)[NW]) {
 }
 
 // Geometry of a warp's smem: a ring of kSlots source rows. A slot holds the
-// 8 planes of the band, each as [4 words left of the band | band words | 4
-// words right of it] (one TMA box), so the +-1 column funnel shifts read the
+// 8 planes of the band, each as [kSlotPad words left of the band | band
+// words | kSlotPad words right of it] (one TMA box), so the +-1 column funnel shifts read the
 // neighbouring lane's (or band's) word straight from shared memory.
+// Words a ring slot holds on either side of the band (the +-1 column moves
+// read one): 4, because a TMA box must start on a 16-byte boundary of the
+// row (a 2-word pad faults with an illegal instruction).
+constexpr int kSlotPad = 4;
 template <int NW, bool FORCE>
 struct Geo {
   static constexpr int kBandWords = 32 * NW;
   static constexpr int kBandCols = 1024 * NW;
-  static constexpr int kPlane = 32 + 4 * kBandWords;
+  static constexpr int kPlane = 4 * (2 * kSlotPad + kBandWords);
   static constexpr int kSlot = 8 * kPlane;
   static constexpr int kSlots = FHPG_PLANES_SLOTS;
   // Output staging (7 planes x band words, the TMA store source) followed by
@@ -285,16 +300,16 @@ __device__ __forceinline__ void rd_shr_e(uint32_t a, uint32_t wp, int lane, uint
 
 // Balanced walk over the set bits of the warp's NW * 32 mask words (word
 // i = lane * NW + w <-> band word i, bit j <-> column 32 i + j of the band).
-// The warp's nonzero words go to a list {mask, key address of the word's
-// first column, sites before it, result word address}; the T sites are
+// The warp's nonzero words go to a list {mask, band column of the word's
+// first bit, sites before it, result word address}; the T sites are
 // split into 32 equal contiguous slices; each lane finds its first word
 // (binary search over the lanes' counts), skips the sites before its slice
 // and visits its sites, advancing through the list (it has no empty words).
-// fn(key address) returns the site's result bit, ORed into the result
+// fn(band column) returns the site's result bit, ORed into the result
 // words (osm). Returns T.
 template <int NW, typename Fn>
 __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint32_t osm,
-                                    uint32_t keys, int lane, Fn&& fn) {
+                                    int lane, Fn&& fn) {
   int cnt = 0, nz = 0;
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
@@ -317,7 +332,7 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
     for (int w = 0; w < NW; ++w) {
       if (m[w]) {
         const uint32_t wi = static_cast<uint32_t>(lane * NW + w);
-        sts128(lsm + q * 16, m[w], keys + wi * 256u, static_cast<uint32_t>(c), osm + wi * 4u);
+        sts128(lsm + q * 16, m[w], wi * 32u, static_cast<uint32_t>(c), osm + wi * 4u);
         ++q;
         c += __popc(m[w]);
       }
@@ -350,7 +365,7 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
     // bit first): skip the slice's predecessors.
     uint32_t mask = en.x, kw = en.y, ow = en.w;
     for (int k = s - static_cast<int>(en.z); k > 0; --k) mask &= mask - 1u;
-    // site: key address, result word address, bit index
+    // site: band column, result word address, bit index
     // j: bit index, v: 1 << j (the result bit's placement is an IMAD with
     // v, FMA pipe, where a shift by j would take the ALU pipe)
     auto next = [&](uint32_t& ka, uint32_t& wa, uint32_t& v) {
@@ -363,7 +378,7 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
       }
       v = mask & (0u - mask);
       mask ^= v;
-      ka = kw + top_bit(v) * 8u;
+      ka = kw + top_bit(v);
       wa = ow;
     };
     int it = s;
@@ -385,16 +400,85 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
   return T;
 }
 
+// Walk variant (FHPG_WALK): 0 = the balanced warp walk above; 1 = every lane
+// visits the set bits of its own NW words, one word after the other,
+// highest bit first, and keeps the result bits in registers (no list, no
+// prefix sums, no slice search, no shared-memory results: fewer
+// instructions per row at the price of the warp waiting for its busiest
+// lane).
+#ifndef FHPG_WALK
+#define FHPG_WALK 1
+#endif
+// fn(band column) returns the site's result as a mask (0 or ~0u).
+template <int NW, typename Fn>
+__device__ __forceinline__ void walk_own(const uint32_t (&m)[NW], int lane, uint32_t (&c)[NW],
+                                         Fn&& fn) {
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    uint32_t mask = m[w], acc = 0u;
+    const uint32_t kw = static_cast<uint32_t>(lane * NW + w) * 32u;
+    while (mask) {
+      const uint32_t j = top_bit(mask);
+      const uint32_t bit = 1u << j;
+      mask ^= bit;
+      acc |= fn(kw + j) & bit;
+    }
+    c[w] = acc;
+  }
+}
+
 template <int NW, bool FORCE>
 struct Ctx {
-  uint32_t kc;      // smem: chirality keys of the band (8 B per column)
-  uint32_t kf;      // smem: forcing keys of the band (8 B per column)
+  // Column keys of the band (fhpg_common.cuh ColKey, key base row ybase):
+  // {lo, t2} (8 B per column) and g (4 B per column), chirality and forcing.
+  uint32_t kc, gc;
+  uint32_t kf, gf;
+  uint32_t ybase;   // global row the band's column keys were made for
+  uint32_t span;    // rows ybase .. ybase + span - 1 use them; later rows hash
+                    // from the step keys (kcur, kfcur)
+  uint32_t x1;      // 1-based lattice column of band column 0
+  uint64_t kcur, kfcur;
   uint32_t four;    // 4, passed at run time (chir_bit)
   uint32_t lsm;     // smem: walk list
   uint32_t osm;     // smem: walk result words
   uint32_t stage;   // smem: output staging (the TMA store source)
   uint64_t thr;
 };
+
+// Builds the band's column keys for columns c0, c0 + dc, ... < ncols (a
+// thread's share) at key base row ybase (global); returns the smallest
+// span among them (every thread of the CTA takes part; the caller reduces).
+template <bool FORCE>
+__device__ __forceinline__ uint32_t make_col_keys(uint32_t kc, uint32_t gc, uint32_t kf,
+                                                  uint32_t gf, uint64_t kcur, uint64_t kfcur,
+                                                  uint32_t x1, uint32_t ybase, int c0, int dc,
+                                                  int ncols) {
+  uint32_t span = 0xFFFFFFFFu;
+  for (int c = c0; c < ncols; c += dc) {
+    const uint64_t x = static_cast<uint64_t>(x1) + c;
+    const ColKey k = col_key_terms(column_key(kcur, x) + ybase);
+    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(kc + c * 8), "r"(k.lo), "r"(k.t2));
+    sts32(gc + c * 4, k.g);
+    span = min(span, colkey_span(k.lo));
+    if (FORCE) {
+      const ColKey f = col_key_terms(column_key(kfcur, x) + ybase);
+      asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(kf + c * 8), "r"(f.lo), "r"(f.t2));
+      sts32(gf + c * 4, f.g);
+      span = min(span, colkey_span(f.lo));
+    }
+  }
+  return span;
+}
+// CTA-wide minimum of the per-thread spans through one slot per warp
+// (slots: 32 words): each warp's lane 0 writes its minimum; after a barrier
+// every thread reads the minimum of all 32 slots.
+__device__ __forceinline__ void span_put(uint32_t slots, uint32_t span) {
+  const uint32_t m = __reduce_min_sync(kFull, span);
+  if ((threadIdx.x & 31) == 0) sts32(slots + (threadIdx.x >> 5) * 4, m);
+}
+__device__ __forceinline__ uint32_t span_get(uint32_t slots) {
+  return __reduce_min_sync(kFull, lds32(slots + (threadIdx.x & 31) * 4));
+}
 
 // One destination row. sm, sc, sn: this lane's word address inside plane 0
 // of the slots of rows r-1, r, r+1; Q = global parity of r.

@@ -64,7 +64,10 @@ namespace {
 // E (the ring kernel, which writes no wrap sectors): the edge reads of
 // rd_shl_e / rd_shr_e; wm, wc, wn: side-buffer rows of source rows r-1, r,
 // r+1 ([8 planes][4 words], E = 1: data words W/32-4 .., E = 2: words 0 ..).
-template <int NW, bool FORCE, int RULE, int Q, int E, bool PADS, typename Rel>
+// FOLD: every row of the call lies inside the column keys' span (the ring
+// kernel re-keys at span boundaries); otherwise rows past it hash from the
+// step keys.
+template <int NW, bool FORCE, int RULE, int Q, int E, bool PADS, bool FOLD, typename Rel>
 __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, uint32_t wm,
                                          uint32_t wc, uint32_t wn, const Ctx<NW, FORCE>& cx,
                                          int lane, uint32_t y, const CUtensorMap* stmap,
@@ -120,22 +123,46 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, 
     K[w] = PlaneRule<RULE>::classify(a, rr[w], so[w]);
     dep[w] = K[w].dep;
   }
+  // Chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y)
+  // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76).
+  // (chir_bit: fin64 bit 0 with fewer ALU-pipe instructions.)
+  uint32_t o[NW][7];
+  // Column keys folded at the band's key base row (fhpg_common.cuh ColKey);
+  // rows past their span (a key's low word would cross a 2^30 block) hash
+  // from the step keys (rare: warp-uniform branch).
+  const uint32_t dy = y - cx.ybase;
+  const bool folded = FOLD || dy < cx.span;
+  auto chir_fast = [&](uint32_t col) -> uint32_t {
+    const uint2 k = lds64v(cx.kc + col * 8u);
+    return chir_mask_pre(k.x + dy, k.y, lds32(cx.gc + col * 4u));
+  };
+  auto chir_slow = [&](uint32_t col) -> uint32_t {
+    return chir_mask(column_key(cx.kcur, cx.x1 + col) + y, cx.four);
+  };
+#if FHPG_WALK == 0
   // The previous row's TMA store must have read the staging area (which
   // also holds the walk scratch) before it is rewritten.
 #if !FHPG_STORE_WAIT_LATE  // timing experiments (1: wait before the outputs, 2: never; wrong results)
   if (lane == 0) bulk_wait_read();
   __syncwarp();
 #endif
-  // Chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y)
-  // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76).
-  // (chir_bit: fin64 bit 0 with fewer ALU-pipe instructions.)
-  const int T = walk<NW>(dep, cx.lsm, cx.osm, cx.kc, lane,
-                         [&](uint32_t ka) { return chir_bit(lds64(ka) + y, cx.four); });
-  uint32_t o[NW][7];
+  const int T = folded ? walk<NW>(dep, cx.lsm, cx.osm, lane,
+                                  [&](uint32_t col) { return chir_fast(col) & 1u; })
+                       : walk<NW>(dep, cx.lsm, cx.osm, lane,
+                                  [&](uint32_t col) { return chir_slow(col) & 1u; });
   const uint32_t mine = cx.osm + lane * NW * 4;
+#else
+  uint32_t cw[NW];
+  if (folded) walk_own<NW>(dep, lane, cw, chir_fast);
+  else walk_own<NW>(dep, lane, cw, chir_slow);
+#endif
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
+#if FHPG_WALK == 0
     const uint32_t c = T ? lds32(mine + w * 4) : 0u;
+#else
+    const uint32_t c = cw[w];
+#endif
     uint32_t oo[6], orr;
     const uint32_t a[6] = {a0[w], a1[w], a2[w], a3[w], a4[w], a5[w]};
     PlaneRule<RULE>::apply(K[w], c, rr[w], a, oo, orr, so[w]);
@@ -148,9 +175,20 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, 
     uint32_t f[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) f[w] = ~so[w] & o[w][5] & ~o[w][2];
-    const int TF = walk<NW>(f, cx.lsm, cx.osm, cx.kf, lane, [&](uint32_t ka) {
-      return (fin64(lds64(ka) + y) >> 32) < cx.thr ? 1u : 0u;
-    });
+    auto force_fast = [&](uint32_t col) -> uint32_t {
+      const uint2 k = lds64v(cx.kf + col * 8u);
+      const uint32_t h = fin64_hi_pre(k.x + dy, k.y, lds32(cx.gf + col * 4u));
+      return static_cast<uint64_t>(h) < cx.thr ? ~0u : 0u;
+    };
+    auto force_slow = [&](uint32_t col) -> uint32_t {
+      const uint32_t h = static_cast<uint32_t>(fin64(column_key(cx.kfcur, cx.x1 + col) + y) >> 32);
+      return static_cast<uint64_t>(h) < cx.thr ? ~0u : 0u;
+    };
+#if FHPG_WALK == 0
+    const int TF = folded ? walk<NW>(f, cx.lsm, cx.osm, lane,
+                                     [&](uint32_t col) { return force_fast(col) & 1u; })
+                          : walk<NW>(f, cx.lsm, cx.osm, lane,
+                                     [&](uint32_t col) { return force_slow(col) & 1u; });
     if (TF) {
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
@@ -160,8 +198,21 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, 
         swaps += __popc(acc);
       }
     }
+#else
+    uint32_t fw[NW];
+    if (folded) walk_own<NW>(f, lane, fw, force_fast);
+    else walk_own<NW>(f, lane, fw, force_slow);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      o[w][5] ^= fw[w];
+      o[w][2] ^= fw[w];
+      swaps += __popc(fw[w]);
+    }
+#endif
   }
-#if FHPG_STORE_WAIT_LATE == 1
+#if FHPG_STORE_WAIT_LATE == 1 || FHPG_WALK != 0
+  // The previous row's TMA store must have read the staging area before it
+  // is rewritten.
   if (lane == 0) bulk_wait_read();
   __syncwarp();
 #endif
@@ -223,7 +274,7 @@ __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap
   const long long pitch = static_cast<long long>(a.pitch);
   const int first = r_begin - 1;  // source rows first .. r_end (local; tensor row = local + 1)
   const int last = r_end;
-  const uint32_t lane_off = 16u + L.lane * NW * 4u;
+  const uint32_t lane_off = 4u * kSlotPad + L.lane * NW * 4u;
   // Ring position of the next row to issue / of rows r-1, r, r+1, and the
   // mbarrier phase of each slot, tracked incrementally.
   uint32_t phase = 0;  // bit k: phase of slot k's next completion
@@ -232,7 +283,7 @@ __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap
     if (L.lane == 0) {
       const uint32_t bar = bars + issue_slot * 8u;
       mbar_expect_tx(bar, G::kRowBytes);
-      tma_row(ring + issue_slot * G::kSlot, map, L.w0 + kPlaneLead - 4, issue_row + 1, bar);
+      tma_row(ring + issue_slot * G::kSlot, map, L.w0 + kPlaneLead - kSlotPad, issue_row + 1, bar);
     }
     ++issue_row;
     issue_slot = issue_slot + 1 == G::kSlots ? 0 : issue_slot + 1;
@@ -250,7 +301,7 @@ __device__ __forceinline__ void run_segment(const StepArgs& a, const CUtensorMap
   auto one = [&](int r, auto qc) {
     constexpr int Q = decltype(qc)::value;
     wait(sn);
-    dest_row<NW, FORCE, RULE, Q, 0, true>(ring + sm * G::kSlot + lane_off,
+    dest_row<NW, FORCE, RULE, Q, 0, true, false>(ring + sm * G::kSlot + lane_off,
                                           ring + sc * G::kSlot + lane_off,
                                           ring + sn * G::kSlot + lane_off, 0u, 0u, 0u, cx, L.lane,
                                           y0 + r, stmap, padmap, L.w0, r + 1, L.padx, swaps, [] {});
@@ -286,11 +337,15 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
   const int seg_group = blockIdx.x / a.nbands_groups;
   const int cta_cols = a.bpc * G::kBandCols;
   const int cta_x0 = band_group * cta_cols;
-  // smem: chirality keys [cta_cols], forcing keys [cta_cols], then per warp
-  // the row ring, the walk list and results, the ring's mbarriers.
+  // smem: chirality column keys ({lo, t2} [cta_cols], g [cta_cols]), the
+  // forcing ones, 32 span slots, then per warp the row ring, the walk list
+  // and results, the ring's mbarriers.
   const uint32_t kc_base = sbase;
-  const uint32_t kf_base = sbase + cta_cols * 8;
-  const uint32_t wbase = sbase + (FORCE ? 2 : 1) * cta_cols * 8 + warp * G::kWarp;
+  const uint32_t gc_base = kc_base + cta_cols * 8;
+  const uint32_t kf_base = gc_base + cta_cols * 4;
+  const uint32_t gf_base = kf_base + cta_cols * 8;
+  const uint32_t slots = sbase + (FORCE ? 2 : 1) * cta_cols * 12;
+  const uint32_t wbase = slots + 128 + warp * G::kWarp;
   const uint32_t ring = wbase;
   const uint32_t stage = ring + G::kSlots * G::kSlot;
   const uint32_t lsm = stage;
@@ -301,12 +356,13 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // Column keys from the step keys (independent of the previous step, so
-  // this overlaps its tail under PDL), then wait for the previous grid.
-  for (int c = threadIdx.x; c < cta_cols; c += blockDim.x) {
-    const uint64_t x = static_cast<uint64_t>(cta_x0 + c) + 1;
-    sts64(kc_base + c * 8, column_key(a.kc_cur, x));
-    if (FORCE) sts64(kf_base + c * 8, column_key(a.kf_cur, x));
-  }
+  // this overlaps its tail under PDL), then wait for the previous grid. Key
+  // base row: the CTA's first row.
+  const uint32_t ybase =
+      static_cast<uint32_t>(a.row0 + a.row_lo + seg_group * a.spc * a.seg_rows);
+  span_put(slots, make_col_keys<FORCE>(kc_base, gc_base, kf_base, gf_base, a.kc_cur, a.kf_cur,
+                                       static_cast<uint32_t>(cta_x0) + 1u, ybase, threadIdx.x,
+                                       blockDim.x, cta_cols));
 #if FHPG_PDL
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -339,7 +395,14 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
   L.padx = (L.w0 + G::kBandWords == L.WW ? 1 : 0) | (L.w0 == 0 ? 2 : 0) | (L.WW << 2);
   Ctx<NW, FORCE> cx;
   cx.kc = kc_base + bic * G::kBandCols * 8;
+  cx.gc = gc_base + bic * G::kBandCols * 4;
   cx.kf = kf_base + bic * G::kBandCols * 8;
+  cx.gf = gf_base + bic * G::kBandCols * 4;
+  cx.ybase = ybase;
+  cx.span = min(span_get(slots), a.span_cap);
+  cx.x1 = static_cast<uint32_t>(cta_x0 + bic * G::kBandCols) + 1u;
+  cx.kcur = a.kc_cur;
+  cx.kfcur = a.kf_cur;
   cx.lsm = lsm;
   cx.osm = osm;
   cx.stage = stage;
@@ -369,11 +432,6 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 // ---------------------------------------------------------------------------
 // Consumer warps per CTA and ring slots (A/B on cfg4: 16/36 1570, 20/44
 // 1695, 24/52 1766, 30/64 1876, 31/48 1889 GSUPS).
-// Back-off of a consumer polling a slot's tag (ns): spinning warps take
-// issue slots from the working ones.
-#ifndef FHPG_TAG_SLEEP
-#define FHPG_TAG_SLEEP 64
-#endif
 // Source rows per TMA box: the producer warp's issue rate (one elected
 // thread: empty-barrier wait, tag, expect_tx, TMA per box) bounds the ring's
 // throughput, so each box carries several rows.
@@ -386,21 +444,8 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 #ifndef FHPG_EXTRA_BUBBLE_ROWS
 #define FHPG_EXTRA_BUBBLE_ROWS 20
 #endif
-#ifndef FHPG_RING_TAGS
-#define FHPG_RING_TAGS 0  // 1: consumers poll per-slot tags before the parity wait
-#endif
 #ifndef FHPG_RING_CONS
 #define FHPG_RING_CONS 31
-#endif
-// Consumers take destination rows from a shared counter (1) instead of the
-// static round-robin (0) (measured: 2097 vs 2111 GSUPS on cfg4, kept off).
-#ifndef FHPG_DYN_ROWS
-#define FHPG_DYN_ROWS 0
-#endif
-// Back-off (ns) of the producer between polls of a ring slot's empty barrier
-// (measured: no effect at 200 or 1000 ns).
-#ifndef FHPG_PROD_SLEEP
-#define FHPG_PROD_SLEEP 0
 #endif
 template <int NW, bool FORCE>
 struct RingGeo {
@@ -409,30 +454,36 @@ struct RingGeo {
 #ifdef FHPG_RING_SLOTS
   static constexpr int kRing = FORCE ? FHPG_RING_SLOTS_F : FHPG_RING_SLOTS;
 #else
-  // Powers of two: the consumer loop divides by the ring and group counts
-  // (the forcing variant's two key tables leave room for 56 slots, but 32
-  // measured 1-3% faster on the forced BASELINE shapes than 56 or 48).
-  static constexpr int kRing = FORCE ? 32 : 64;
+  // Any multiple of the box rows: the consumers track slot indices
+  // incrementally. 56 is what the folded column keys leave room for
+  // (forcing: 32, 1-3% faster on the forced BASELINE shapes than 56 or 48
+  // before the folded keys).
+  static constexpr int kRing = FORCE ? 32 : 56;
 #endif
   static constexpr int kThreads = (kCons + 1) * 32;
-  static constexpr int kKeys = (FORCE ? 2 : 1) * G::kBandCols * 8;
+  // Column keys: {lo, t2} and g per column (chirality, then forcing), then
+  // 32 span slots.
+  static constexpr int kKeyTab = G::kBandCols * 12;
+  static constexpr int kSpanOff = (FORCE ? 2 : 1) * kKeyTab;
+  static constexpr int kKeys = kSpanOff + 128;
   static constexpr int kRingOff = (kKeys + 127) / 128 * 128;
   static constexpr int kStageOff = kRingOff + kRing * G::kSlot;
   static constexpr int kBarOff = kStageOff + kCons * G::kStage;  // (no wrap-sector box)
-  static constexpr int kTagOff = kBarOff + 2 * 8 * kRing;
-  static constexpr int kCtrOff = kTagOff + 4 * kRing;  // dynamic row counters (2 parts)
   static constexpr int kBox = FHPG_BOX_ROWS;     // source rows per TMA box (a "group")
   static constexpr int kGroups = kRing / kBox;   // ring slots of whole groups
   static_assert(kRing % kBox == 0, "row groups");
-  // Full barriers, one per group modulo 4 kGroups. A consumer waiting on
-  // group P has finished its previous row (31 rows = at most 9 groups back),
-  // so the producer has issued group P - 9 and with it every group up to
-  // P - 9 - kGroups has been consumed: the barrier's use for group
-  // P - 4 kGroups is complete and the parity wait for group P is unambiguous
-  // (no slot tags). Needs the static row assignment (FHPG_DYN_ROWS 0).
-  static constexpr int kFullBars = 4 * kGroups;
-  static_assert(kFullBars <= kRing, "full barriers fit the per-slot allocation");
-  static_assert(FHPG_RING_TAGS || (kCons <= 31 && !FHPG_DYN_ROWS), "tag-free ring bound");
+  static_assert((kBox & (kBox - 1)) == 0, "box rows: a power of two");
+  // Full barriers, one per group modulo kFullBars (a power of two >= 4
+  // kGroups). A consumer waiting on group P has finished its previous row
+  // (31 rows = at most 9 groups back), so the producer has issued group
+  // P - 9 and with it every group up to P - 9 - kGroups has been consumed:
+  // the barrier's use for group P - kFullBars is complete and the parity
+  // wait for group P is unambiguous (static round-robin rows, no slot tags).
+  static constexpr int kFullBars = kGroups <= 8 ? 32 : kGroups <= 16 ? 64 : 128;
+  static_assert(kFullBars > kGroups + (kCons + kBox) / kBox + 1, "tag-free ring bound");
+  static_assert(kCons <= 31, "consumer warps");
+  // mbarriers: kFullBars full, kGroups empty.
+  static constexpr int kCtrOff = kBarOff + 8 * (kFullBars + kGroups);
   // Side buffer of the edge bands: per group, the 4 data words across the
   // periodic wrap of every plane and row ([kBox rows][8 planes][4 words]).
   static constexpr int kSideGroup = kBox * 8 * 16;
@@ -440,6 +491,23 @@ struct RingGeo {
   static constexpr int kSmem = kSideOff + kGroups * kSideGroup;
   static_assert(kSmem <= 232448, "shared memory per CTA");
 };
+
+// Re-keying by the consumer warps of a ring CTA (barrier 2): once every
+// consumer is past the rows of the current keys, the band's column keys are
+// rebuilt for key base row ybase (a band switch, or rows reaching the
+// keys' span); returns the new span. Not inlined: it runs a few times per
+// thousand CTA steps.
+template <bool FORCE, int NCONS, int NCOLS>
+__device__ __noinline__ uint32_t rekey_consumers(uint32_t kc, uint32_t gc, uint32_t kf, uint32_t gf,
+                                                 uint32_t slots, uint64_t kcur, uint64_t kfcur,
+                                                 uint32_t x1, uint32_t ybase) {
+  asm volatile("bar.sync 2, %0;" ::"n"(NCONS) : "memory");
+  span_put(slots, make_col_keys<FORCE>(kc, gc, kf, gf, kcur, kfcur, x1, ybase, threadIdx.x, NCONS,
+                                       NCOLS));
+  if (threadIdx.x == 0) sts32(slots + (NCONS / 32) * 4, 0xFFFFFFFFu);  // the producer's slot
+  asm volatile("bar.sync 2, %0;" ::"n"(NCONS) : "memory");
+  return span_get(slots);
+}
 
 __device__ __forceinline__ void mbar_arrive(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -486,41 +554,35 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   // (row_lo-1 .. row_lo+nB) from the next whole group on.
   const uint32_t offB = (static_cast<uint32_t>(nA) + 2 + B - 1) / B * B;
   const uint32_t kc_base = sbase;
-  const uint32_t kf_base = sbase + G::kBandCols * 8;
+  const uint32_t gc_base = kc_base + G::kBandCols * 8;
+  const uint32_t kf_base = kc_base + RG::kKeyTab;
+  const uint32_t gf_base = kf_base + G::kBandCols * 8;
+  const uint32_t slots = sbase + RG::kSpanOff;
   const uint32_t ring = sbase + RG::kRingOff;
   const uint32_t full = sbase + RG::kBarOff;
-  const uint32_t empty = full + 8 * RG::kRing;
+  const uint32_t empty = full + 8 * RG::kFullBars;
   const uint32_t side = sbase + RG::kSideOff;
   // Which wrap a band's rows need from the side buffer (1: band 0 of several,
   // 2: the last band of several; a single band finds both in its own box).
   auto edge_of = [&](int b) { return a.nbands == 1 ? 3 : b == 0 ? 1 : b == a.nbands - 1 ? 2 : 0; };
-  // tag[k] = ring index of the row the producer last issued into slot k. A
-  // consumer visits only every kCons-th row, so a bare parity wait could
-  // mistake a slot two phases old for the one it needs; it first waits for
-  // the tag, after which the full barrier's parity is unambiguous.
-  const uint32_t tags = sbase + RG::kTagOff;
   if (threadIdx.x == 0) {
-    for (int k = 0; k < RG::kRing; ++k) {
-      // Source rows come in groups of kBox (one TMA box): group P = index /
-      // kBox uses barriers / tag P mod kGroups (3 consumers per row).
-      mbar_init(full + k * 8, 1);
-      mbar_init(empty + k * 8, 3 * RG::kBox);
-      sts32(tags + k * 4, 0xFFFFFFFFu);
-    }
-    sts32(sbase + RG::kCtrOff, 0u);
-    sts32(sbase + RG::kCtrOff + 4, 0u);
+    // Source rows come in groups of kBox (one TMA box): group P = index /
+    // kBox fills ring group P mod kGroups, completes full barrier P mod
+    // kFullBars and is released on empty barrier P mod kGroups (3 consumers
+    // per row).
+    for (int k = 0; k < RG::kFullBars; ++k) mbar_init(full + k * 8, 1);
+    for (int k = 0; k < RG::kGroups; ++k) mbar_init(empty + k * 8, 3 * RG::kBox);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // The band's column keys, made here from the step keys (they depend on
   // nothing the previous step wrote, so this overlaps its tail under PDL).
-  auto make_keys = [&](int b, int t0, int nt) {
-    for (int c = t0; c < G::kBandCols; c += nt) {
-      const uint64_t x = static_cast<uint64_t>(b * G::kBandCols + c) + 1;
-      sts64(kc_base + c * 8, column_key(a.kc_cur, x));
-      if (FORCE) sts64(kf_base + c * 8, column_key(a.kf_cur, x));
-    }
+  // Key base row: the part's first destination row.
+  auto make_keys = [&](int b, uint32_t ybase, int t0, int nt) {
+    span_put(slots, make_col_keys<FORCE>(kc_base, gc_base, kf_base, gf_base, a.kc_cur, a.kf_cur,
+                                         static_cast<uint32_t>(b * G::kBandCols) + 1u, ybase, t0,
+                                         nt, G::kBandCols));
   };
-  make_keys(bA, threadIdx.x, blockDim.x);
+  make_keys(bA, static_cast<uint32_t>(a.row0 + RA0), threadIdx.x, blockDim.x);
 #if FHPG_PDL
   // Let the next step's grid launch now; wait for the previous step's grid
   // (the lattice rows it wrote, the key buffers it read) before going on.
@@ -542,33 +604,13 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
       constexpr uint32_t kG = RG::kGroups;
       const uint32_t gA = offB / B;
       const uint32_t ngroups = gA + (nB > 0 ? (static_cast<uint32_t>(nB) + 2 + B - 1) / B : 0u);
+      // k = P mod kG (ring group), lap = P / kG, tracked incrementally
+      uint32_t k = 0, lap = 0;
       for (uint32_t P = 0; P < ngroups; ++P) {
-        const uint32_t k = P % kG;
-        if (P >= kG) {
-#if FHPG_PROD_SLEEP
-          uint32_t done;
-          for (;;) {
-            asm volatile(
-                "{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                : "=r"(done) : "r"(empty + k * 8), "r"((P / kG - 1) & 1u) : "memory");
-            if (done) break;
-            __nanosleep(FHPG_PROD_SLEEP);
-          }
-#else
-          mbar_wait(empty + k * 8, (P / kG - 1) & 1u);
-#endif
-        }
-#if FHPG_RING_TAGS
-        {  // tag: an atomic store (consumers poll it; not a data race)
-          uint32_t prev;
-          asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(prev) : "r"(tags + k * 4), "r"(P) : "memory");
-        }
-        const uint32_t fb = full + k * 8;
-#else
+        if (lap > 0) mbar_wait(empty + k * 8, (lap - 1) & 1u);
         const uint32_t fb = full + (P % RG::kFullBars) * 8;
-#endif
         const bool inA = P < gA;
-        const int word = (inA ? bA : bA + 1) * G::kBandWords + kPlaneLead - 4;  // band - 4 words
+        const int word = (inA ? bA : bA + 1) * G::kBandWords + kPlaneLead - kSlotPad;
         const int trow = inA ? RA0 + static_cast<int>(B * P) : row_lo + static_cast<int>(B * P - offB);
 #if FHPG_STREAM_ONLY == 3 || FHPG_STREAM_ONLY >= 5  // timing experiments: no loads
         if (FHPG_STREAM_ONLY >= 5 && P < kG) {  // 5, 6: compute on the first ring fill
@@ -591,6 +633,10 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
         // slot is never freed.
         if (nB > 0 && P + 1 == gA && offB > static_cast<uint32_t>(nA) + 2)
           mbar_arrive(empty + k * 8, 3 * (offB - static_cast<uint32_t>(nA) - 2));
+        if (++k == kG) {
+          k = 0;
+          ++lap;
+        }
       }
     }
     return;
@@ -608,64 +654,75 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   const uint32_t stage = sbase + RG::kStageOff + warp * G::kStage;
   Ctx<NW, FORCE> cx;
   cx.kc = kc_base;
+  cx.gc = gc_base;
   cx.kf = kf_base;
+  cx.gf = gf_base;
+  cx.ybase = static_cast<uint32_t>(a.row0 + RA0);
+  cx.span = max(1u, min(span_get(slots), a.span_cap));
+  cx.x1 = static_cast<uint32_t>(bA * G::kBandCols) + 1u;
+  cx.kcur = a.kc_cur;
+  cx.kfcur = a.kf_cur;
   cx.lsm = stage;
   cx.osm = stage + G::kList;
   cx.stage = stage;
   cx.thr = a.thr;
   cx.four = a.k4;
   unsigned swaps = 0;
-  const uint32_t lane_off = 16u + lane * NW * 4u;
+  const uint32_t lane_off = 4u * kSlotPad + lane * NW * 4u;
   const uint32_t y0 = static_cast<uint32_t>(a.row0);  // global rows < 2^31
   // Destination rows [Rb, Re) of the current band, warp-interleaved; source
   // row r - 1 sits at ring index ibase + r - Rb. Inlined once per part (one
   // copy inside a loop over the parts measured 8% slower: spills).
-  auto rows = [&](auto ec, const int Rb, const int Re, const uint32_t ibase,
+  // Column keys are valid for rows [key_row, key_row + span) of the band;
+  // reaching the end re-keys (all consumers, rekey_consumers).
+  int key_row = RA0;
+  auto key_end = [&](int Re) { return key_row + static_cast<int>(min(cx.span, static_cast<uint32_t>(Re - key_row))); };
+  auto rekey = [&](int b, int row) {
+    cx.span = max(1u, min(rekey_consumers<FORCE, RG::kCons * 32, G::kBandCols>(
+                              kc_base, gc_base, kf_base, gf_base, slots, a.kc_cur, a.kf_cur,
+                              static_cast<uint32_t>(b * G::kBandCols) + 1u,
+                              y0 + static_cast<uint32_t>(row)),
+                          a.span_cap));
+    cx.ybase = y0 + static_cast<uint32_t>(row);
+    key_row = row;
+  };
+  auto rows = [&](auto ec, const int b, const int Rb, const int Re, const uint32_t ibase,
                   const uint32_t ctr) __attribute__((always_inline)) {
     constexpr int E = decltype(ec)::value;
-#if FHPG_DYN_ROWS
-    for (;;) {
-      int r = 0;
-      if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(r) : "r"(ctr) : "memory");
-      r = Rb + __shfl_sync(kFull, r, 0);
-      if (r >= Re) break;
-#else
+    int kend = key_end(Re);
     (void)ctr;
-    for (int r = Rb + warp; r < Re; r += RG::kCons) {
-#endif
-      const uint32_t i = ibase + static_cast<uint32_t>(r - Rb);  // ring index of source row r - 1
+    // Ring index i of source row r - 1 and its slot s0 = i mod kRing, both
+    // advanced by kCons per row of this warp.
+    uint32_t i = ibase + static_cast<uint32_t>(warp);
+    uint32_t s0 = i % RG::kRing;
+    auto wrap = [](uint32_t x) { return x >= static_cast<uint32_t>(RG::kRing) ? x - RG::kRing : x; };
+    for (int r = Rb + warp; r < Re;
+         r += RG::kCons, i += RG::kCons, s0 = wrap(s0 + RG::kCons)) {
+      while (r >= kend) {  // rows past the keys' span: re-key at kend
+        rekey(b, kend);
+        kend = key_end(Re);
+      }
       const bool first_row = r == Rb, last_row = r == Re - 1;
-      constexpr uint32_t kG = RG::kGroups;
+      const uint32_t sd[3] = {s0, wrap(s0 + 1), wrap(s0 + 2)};
       uint32_t sl[3];
 #pragma unroll
       for (uint32_t d = 0; d < 3; ++d) {
-        const uint32_t P = (i + d) / B;
-        if (d == 0 || ((i + d) % B) == 0) {  // a new group
-#if FHPG_RING_TAGS
-          const uint32_t kp = P % kG;
-          for (;;) {
-            uint32_t tag;
-            asm volatile("ld.relaxed.cta.shared.u32 %0, [%1];"
-                         : "=r"(tag) : "r"(tags + kp * 4) : "memory");
-            if (tag == P) break;
-            __nanosleep(FHPG_TAG_SLEEP);
-          }
-          mbar_wait(full + kp * 8, (P / kG) & 1u);
-#else
+        if (d == 0 || (sd[d] % B) == 0) {  // a new group
+          const uint32_t P = (i + d) / B;
           mbar_wait(full + (P % RG::kFullBars) * 8, (P / RG::kFullBars) & 1u);
-#endif
         }
-        sl[d] = ring + ((i + d) % RG::kRing) * G::kSlot + lane_off;
+        sl[d] = ring + sd[d] * G::kSlot + lane_off;
       }
       uint32_t sw[3] = {0u, 0u, 0u};  // side-buffer rows of the source rows
       if constexpr (E == 1 || E == 2) {
+        static_assert(RG::kSideGroup == B * 8 * 16, "side rows");
 #pragma unroll
-        for (uint32_t d = 0; d < 3; ++d)
-          sw[d] = side + ((i + d) / B % kG) * RG::kSideGroup + ((i + d) % B) * (8u * 16u);
+        for (uint32_t d = 0; d < 3; ++d) sw[d] = side + sd[d] * (8u * 16u);
       }
       // Release the three source rows as soon as they are in registers (3
       // consumers per row; segment edges make up for the destination rows
-      // outside [Rb, Re)); one arrive per group the rows fall in.
+      // outside [Rb, Re)); one arrive per group the rows fall in (ring group
+      // of slot s = s / B).
       auto release = [&] {
         __syncwarp();
         if (lane == 0) {
@@ -673,41 +730,44 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
           const uint32_t c0 = 1 + 2 * first, c1 = 1 + first + lastr, c2 = 1 + 2 * lastr;
           const uint32_t g0 = i / B, g1 = (i + 1) / B, g2 = (i + 2) / B;
           if (g0 == g2) {
-            mbar_arrive(empty + (g0 % kG) * 8, c0 + c1 + c2);
+            mbar_arrive(empty + (sd[0] / B) * 8, c0 + c1 + c2);
           } else {
-            mbar_arrive(empty + (g0 % kG) * 8, c0 + (g1 == g0 ? c1 : 0u));
-            mbar_arrive(empty + (g2 % kG) * 8, c2 + (g1 == g2 ? c1 : 0u));
+            mbar_arrive(empty + (sd[0] / B) * 8, c0 + (g1 == g0 ? c1 : 0u));
+            mbar_arrive(empty + (sd[2] / B) * 8, c2 + (g1 == g2 ? c1 : 0u));
           }
         }
       };
       if ((a.row0 + r) & 1)
-        dest_row<NW, FORCE, RULE, 1, E, false>(sl[0], sl[1], sl[2], sw[0], sw[1], sw[2], cx, lane,
+        dest_row<NW, FORCE, RULE, 1, E, false, true>(sl[0], sl[1], sl[2], sw[0], sw[1], sw[2], cx, lane,
                                                y0 + r, &stmap, nullptr, L.w0, r + 1, 0, swaps,
                                                release);
       else
-        dest_row<NW, FORCE, RULE, 0, E, false>(sl[0], sl[1], sl[2], sw[0], sw[1], sw[2], cx, lane,
+        dest_row<NW, FORCE, RULE, 0, E, false, true>(sl[0], sl[1], sl[2], sw[0], sw[1], sw[2], cx, lane,
                                                y0 + r, &stmap, nullptr, L.w0, r + 1, 0, swaps,
                                                release);
       }
+    while (kend < Re) {  // re-keyings the other consumers still take part in
+      rekey(b, kend);
+      kend = key_end(Re);
+    }
   };
   // One inlined copy of the row loop per edge kind (interior bands pay
   // nothing for the wrap).
   auto rows_e = [&](int b, const int Rb, const int Re, const uint32_t ibase,
                     const uint32_t ctr) __attribute__((always_inline)) {
     switch (edge_of(b)) {
-      case 0: rows(std::integral_constant<int, 0>{}, Rb, Re, ibase, ctr); break;
-      case 1: rows(std::integral_constant<int, 1>{}, Rb, Re, ibase, ctr); break;
-      case 2: rows(std::integral_constant<int, 2>{}, Rb, Re, ibase, ctr); break;
-      default: rows(std::integral_constant<int, 3>{}, Rb, Re, ibase, ctr); break;
+      case 0: rows(std::integral_constant<int, 0>{}, b, Rb, Re, ibase, ctr); break;
+      case 1: rows(std::integral_constant<int, 1>{}, b, Rb, Re, ibase, ctr); break;
+      case 2: rows(std::integral_constant<int, 2>{}, b, Rb, Re, ibase, ctr); break;
+      default: rows(std::integral_constant<int, 3>{}, b, Rb, Re, ibase, ctr); break;
     }
   };
   rows_e(bA, RA0, RA0 + nA, 0u, sbase + RG::kCtrOff);
   if (nB > 0) {
     // Extra CTA: on to band bA + 1 once every consumer is done with band bA
     // (the key table is rewritten); the producer streams on meanwhile.
-    asm volatile("bar.sync 1, %0;" ::"r"(RG::kCons * 32) : "memory");
-    make_keys(bA + 1, threadIdx.x, RG::kCons * 32);
-    asm volatile("bar.sync 1, %0;" ::"r"(RG::kCons * 32) : "memory");
+    rekey(bA + 1, row_lo);
+    cx.x1 = static_cast<uint32_t>((bA + 1) * G::kBandCols) + 1u;
     set_band(bA + 1);
     rows_e(bA + 1, row_lo, row_lo + nB, offB, sbase + RG::kCtrOff + 4);
   }
@@ -795,7 +855,7 @@ void launch_ring(StepArgs a, const CUtensorMap* src, const CUtensorMap* dst, int
 template <int NW, bool FORCE>
 int smem_bytes(int bpc) {
   using G = Geo<NW, FORCE>;
-  return (FORCE ? 2 : 1) * bpc * G::kBandCols * 8 + kPWarps<NW> * G::kWarp;
+  return (FORCE ? 2 : 1) * bpc * G::kBandCols * 12 + 128 + kPWarps<NW> * G::kWarp;
 }
 
 template <int NW, bool FORCE, int RULE>
@@ -959,7 +1019,7 @@ bool make_planes_map(void* tmap, uint8_t* buffer, int W, size_t pitch, int rows,
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(xw * 4), static_cast<cuuint64_t>(pitch)};
   const bool load = kind == kMapLoad || kind == kMapLoadRows || kind == kMapSide;
   const cuuint32_t box[3] = {
-      static_cast<cuuint32_t>(kind == kMapSide ? 4 : load ? 32 * nw + 8
+      static_cast<cuuint32_t>(kind == kMapSide ? 4 : load ? 32 * nw + 2 * kSlotPad
                               : kind == kMapPad ? kPlaneWrap : 32 * nw),
       load ? 8u : 7u,
       kind == kMapLoadRows || kind == kMapSide ? static_cast<cuuint32_t>(FHPG_BOX_ROWS) : 1u};

@@ -107,16 +107,16 @@ __device__ __forceinline__ void resident_row(uint32_t sm, uint32_t sc, uint32_t 
   const auto K = PlaneRule<RULE>::classify(a, rr[0], so[0]);
   const uint32_t dep[1] = {K.dep};
   // chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y) (step.cpp:73-76)
-  const int T = walk<1>(dep, lsm, osm, kc, lane,
-                        [&](uint32_t ka) { return chir_bit(lds64(ka) + y, four); });
+  const int T = walk<1>(dep, lsm, osm, lane,
+                        [&](uint32_t col) { return chir_bit(lds64(kc + col * 8u) + y, four); });
   const uint32_t c = T ? lds32(osm + lane * 4) : 0u;
   uint32_t o[7];
   PlaneRule<RULE>::apply(K, c, rr[0], a, o, o[6], so[0]);
   if constexpr (FORCE) {
     // step.cpp:79-88: fluid, W (bit 5) set, E (bit 2) clear after collision
     const uint32_t f[1] = {~so[0] & o[5] & ~o[2]};
-    const int TF = walk<1>(f, lsm, osm, kf, lane, [&](uint32_t ka) {
-      return (fin64(lds64(ka) + y) >> 32) < thr ? 1u : 0u;
+    const int TF = walk<1>(f, lsm, osm, lane, [&](uint32_t col) {
+      return (fin64(lds64(kf + col * 8u) + y) >> 32) < thr ? 1u : 0u;
     });
     if (TF) {
       const uint32_t acc = lds32(osm + lane * 4);

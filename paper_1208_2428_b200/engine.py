@@ -69,6 +69,7 @@ SIGNATURES = {
                             C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), u64p]),
     "fhpg_force_generic": (C.c_int, [C.c_void_p, C.c_int]),
     "fhpg_select_path": (C.c_int, [C.c_void_p, C.c_int]),
+    "fhpg_debug_key_span": (C.c_int, [C.c_void_p, C.c_uint32]),
     "fhpg_resident_depth": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_int)]),
     # include/fhpg_tables.h
     "fhpg_build_table": (C.c_int, [C.c_int, u8p]),
@@ -250,6 +251,11 @@ class Engine:
 
     def force_generic(self, on: bool = True):
         _check(self.lib.fhpg_force_generic(self.h, int(on)))
+
+    def debug_key_span(self, rows: int = 0xFFFFFFFF):
+        """Testing aid: cap the rows per column-key base of the bit-plane
+        kernels (re-keying / step-key hashing past it); results unchanged."""
+        _check(self.lib.fhpg_debug_key_span(self.h, rows))
 
     def set_table(self, table):
         t = _u8(table)

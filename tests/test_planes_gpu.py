@@ -219,10 +219,12 @@ def _mix64_np(z):
     return z ^ (z >> np.uint64(31))
 
 
-def _carry_steps(seed, W, H, want, limit=200000):
+def _carry_steps(seed, W, H, want, limit=200000, block=1 << 32):
     """Steps whose chirality column keys have a low word that carries for
     some row y in 1..H-1 but not for row 0 (lo32(K) > 2^32 - H), where
-    key + y must carry into the high word (rng.hpp:25-33)."""
+    key + y must carry into the high word (rng.hpp:25-33). With block =
+    2^30: keys whose low word leaves its 2^30 block inside the rows (where
+    the bit-plane kernels' folded column keys end and they re-key)."""
     base = int(_mix64_np(np.array([(seed + _GAMMA * 2) & _M64], np.uint64))[0])
     xs = np.arange(1, W + 1, dtype=np.uint64)
     found = []
@@ -231,8 +233,8 @@ def _carry_steps(seed, W, H, want, limit=200000):
             st = np.arange(s0, s0 + 4096, dtype=np.uint64)
             sk = _mix64_np(np.uint64(base) + st)
             keys = _mix64_np(sk[:, None] + xs[None, :]) + np.uint64(_GAMMA)
-            lo = keys & np.uint64(0xFFFFFFFF)
-            hit = np.argwhere(lo > np.uint64((1 << 32) - H))
+            lo = keys & np.uint64(block - 1)
+            hit = np.argwhere(lo > np.uint64(block - H))
             for r, c in hit:
                 found.append((int(st[r]), int(c)))
             if len({f[0] for f in found}) >= want:
@@ -259,6 +261,46 @@ def test_ring_carry_columns(port, tables):
         out = e.download()
         assert (out == ref).all(), (st, [f for f in found if f[0] == st], np.argwhere(out != ref)[:5])
 
+
+
+def test_ring_key_block_crossing(port, tables):
+    """Steps where some column key's low word leaves its 2^30 block between
+    two rows of the lattice: the ring kernel's folded column keys (ColKey,
+    valid while lo + dy stays in the block) end there and the consumers
+    re-key the band at that row (rekey_consumers)."""
+    W, H, seed = 4096, 1000, 78
+    steps, found = _carry_steps(seed, W, H, want=6, block=1 << 30)
+    assert len(steps) >= 3
+    s = np.full((H, W), 0x09, np.uint8)
+    m = np.zeros((H, W), np.uint8)
+    e = engine(W, H, tables["fhp3"], m, s)
+    assert e.path == "planes"
+    for st in steps:
+        e.upload(s)
+        e.advance(seed, 0.0, st, 1)
+        ref, _ = port.advance(s, tables["fhp3"], seed, 0, st, 1, mask=m)
+        out = e.download()
+        assert (out == ref).all(), (st, [f for f in found if f[0] == st], np.argwhere(out != ref)[:5])
+
+
+@pytest.mark.parametrize("W,H,fp,cap", [(16384, 1100, 0.3, 1), (16384, 1100, 0.0, 37),
+                                        (4096, 131, 0.3, 0), (4096, 131, 1.0, 5),
+                                        (3072, 64, 0.3, 0), (3072, 64, 0.0, 7),
+                                        (1024, 64, 0.3, 3), (2048, 37, 0.01, 2)])
+def test_key_span_cap(W, H, fp, cap, port, tables):
+    """Column-key spans capped (fhpg_debug_key_span): the ring kernel re-keys
+    every `cap` rows (cap 0 acts as 1), incl. across the extra CTAs' band
+    switch; the per-warp kernel (W = 1024 x odd) hashes the rows past the
+    cap from the step keys. Results are identical to the oracle."""
+    s, m = port.scramble(W, H, W * 3 + H + cap)
+    e = engine(W, H, tables["fhp3"], m, s, path="streaming")
+    assert e.path == "planes"
+    e.debug_key_span(cap)
+    sw = e.advance(5, fp, 1234, 3)
+    ref, rsw = port.advance(s, tables["fhp3"], 5, port.threshold(fp), 1234, 3, mask=m)
+    out = e.download()
+    assert (out == ref).all(), np.argwhere(out != ref)[:5]
+    assert sw == rsw
 
 
 @pytest.mark.parametrize("W,H,fp", [(16384, 1100, 0.0), (16384, 1100, 0.3), (12288, 1500, 0.05),

@@ -22,3 +22,4 @@ def test_planes_circuits_match_tables(tmp_path):
     assert "default: ok (3 dep states)" in out.stdout
     assert "fhp1: ok (3 dep states)" in out.stdout
     assert "chir_bit: ok" in out.stdout
+    assert "col_key_terms: ok" in out.stdout

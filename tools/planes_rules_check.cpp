@@ -113,5 +113,28 @@ int main() {
     std::printf("chir_bit: %s (%ld keys)\n", wrong ? "MISMATCH" : "ok", n);
     bad += wrong != 0;
   }
+  // Folded column terms (col_key_terms / chir_mask_pre / fin64_hi_pre) ==
+  // fin64(K + dy) for every dy inside colkey_span: random keys, and keys at
+  // the end of a 2^30 block (span 1 .. 256).
+  {
+    uint64_t st = 0x13198A2E03707344ull;
+    long n = 0, wrong = 0;
+    for (int i = 0; i < 1000000; ++i) {
+      st = mix64(st);
+      uint64_t K = st;
+      if (i % 2) K = (K & ~0x3FFFFFFFull) | (0x3FFFFFFFull - (mix64(st ^ 7) & 0xFF));
+      const ColKey c = col_key_terms(K);
+      const uint32_t span = colkey_span(c.lo);
+      uint32_t dy = static_cast<uint32_t>(mix64(st ^ 3) >> 44);  // < 2^20
+      if (i % 2 || dy >= span) dy = span - 1 - (dy % (span < 64 ? span : 64));
+      const uint64_t f = fin64(K + dy);
+      ++n;
+      if (chir_mask_pre(c.lo + dy, c.t2, c.g) != ((f & 1u) ? ~0u : 0u) ||
+          fin64_hi_pre(c.lo + dy, c.t2, c.g) != static_cast<uint32_t>(f >> 32))
+        ++wrong;
+    }
+    std::printf("col_key_terms: %s (%ld keys)\n", wrong ? "MISMATCH" : "ok", n);
+    bad += wrong != 0;
+  }
   return bad ? 1 : 0;
 }
