@@ -413,6 +413,38 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
 template <int NW, typename Fn>
 __device__ __forceinline__ void walk_own(const uint32_t (&m)[NW], int lane, uint32_t (&c)[NW],
                                          Fn&& fn) {
+  if constexpr (NW == 2) {
+    // The warp waits for its busiest lane in each of the two word loops:
+    // every lane takes its fuller word first, so the first loop's maximum
+    // is over the fuller words and the second's over the emptier ones
+    // (expected 15.0 instead of 16.6 iterations at 12.6% dep sites).
+    const bool sw = __popc(m[1]) > __popc(m[0]);
+    const uint32_t kw = static_cast<uint32_t>(lane * 2) * 32u;
+    uint32_t acc0 = 0u, acc1 = 0u;
+    {
+      uint32_t mask = sw ? m[1] : m[0];
+      const uint32_t k0 = kw + (sw ? 32u : 0u);
+      while (mask) {
+        const uint32_t j = top_bit(mask);
+        const uint32_t bit = 1u << j;
+        mask ^= bit;
+        acc0 |= fn(k0 + j) & bit;
+      }
+    }
+    {
+      uint32_t mask = sw ? m[0] : m[1];
+      const uint32_t k1 = kw + (sw ? 0u : 32u);
+      while (mask) {
+        const uint32_t j = top_bit(mask);
+        const uint32_t bit = 1u << j;
+        mask ^= bit;
+        acc1 |= fn(k1 + j) & bit;
+      }
+    }
+    c[0] = sw ? acc1 : acc0;
+    c[1] = sw ? acc0 : acc1;
+    return;
+  }
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
     uint32_t mask = m[w], acc = 0u;
@@ -430,9 +462,9 @@ __device__ __forceinline__ void walk_own(const uint32_t (&m)[NW], int lane, uint
 template <int NW, bool FORCE>
 struct Ctx {
   // Column keys of the band (fhpg_common.cuh ColKey, key base row ybase):
-  // {lo, t2} (8 B per column) and g (4 B per column), chirality and forcing.
-  uint32_t kc, gc;
-  uint32_t kf, gf;
+  // {lo, t2, g, 0} per column (one 16-byte load), chirality and forcing.
+  uint32_t kc;
+  uint32_t kf;
   uint32_t ybase;   // global row the band's column keys were made for
   uint32_t span;    // rows ybase .. ybase + span - 1 use them; later rows hash
                     // from the step keys (kcur, kfcur)
@@ -449,21 +481,18 @@ struct Ctx {
 // thread's share) at key base row ybase (global); returns the smallest
 // span among them (every thread of the CTA takes part; the caller reduces).
 template <bool FORCE>
-__device__ __forceinline__ uint32_t make_col_keys(uint32_t kc, uint32_t gc, uint32_t kf,
-                                                  uint32_t gf, uint64_t kcur, uint64_t kfcur,
-                                                  uint32_t x1, uint32_t ybase, int c0, int dc,
-                                                  int ncols) {
+__device__ __forceinline__ uint32_t make_col_keys(uint32_t kc, uint32_t kf, uint64_t kcur,
+                                                  uint64_t kfcur, uint32_t x1, uint32_t ybase,
+                                                  int c0, int dc, int ncols) {
   uint32_t span = 0xFFFFFFFFu;
   for (int c = c0; c < ncols; c += dc) {
     const uint64_t x = static_cast<uint64_t>(x1) + c;
     const ColKey k = col_key_terms(column_key(kcur, x) + ybase);
-    asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(kc + c * 8), "r"(k.lo), "r"(k.t2));
-    sts32(gc + c * 4, k.g);
+    sts128(kc + c * 16, k.lo, k.t2, k.g, 0u);
     span = min(span, colkey_span(k.lo));
     if (FORCE) {
       const ColKey f = col_key_terms(column_key(kfcur, x) + ybase);
-      asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(kf + c * 8), "r"(f.lo), "r"(f.t2));
-      sts32(gf + c * 4, f.g);
+      sts128(kf + c * 16, f.lo, f.t2, f.g, 0u);
       span = min(span, colkey_span(f.lo));
     }
   }

@@ -133,8 +133,8 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, 
   const uint32_t dy = y - cx.ybase;
   const bool folded = FOLD || dy < cx.span;
   auto chir_fast = [&](uint32_t col) -> uint32_t {
-    const uint2 k = lds64v(cx.kc + col * 8u);
-    return chir_mask_pre(k.x + dy, k.y, lds32(cx.gc + col * 4u));
+    const uint4 k = lds128(cx.kc + col * 16u);
+    return chir_mask_pre(k.x + dy, k.y, k.z);
   };
   auto chir_slow = [&](uint32_t col) -> uint32_t {
     return chir_mask(column_key(cx.kcur, cx.x1 + col) + y, cx.four);
@@ -176,8 +176,8 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, 
 #pragma unroll
     for (int w = 0; w < NW; ++w) f[w] = ~so[w] & o[w][5] & ~o[w][2];
     auto force_fast = [&](uint32_t col) -> uint32_t {
-      const uint2 k = lds64v(cx.kf + col * 8u);
-      const uint32_t h = fin64_hi_pre(k.x + dy, k.y, lds32(cx.gf + col * 4u));
+      const uint4 k = lds128(cx.kf + col * 16u);
+      const uint32_t h = fin64_hi_pre(k.x + dy, k.y, k.z);
       return static_cast<uint64_t>(h) < cx.thr ? ~0u : 0u;
     };
     auto force_slow = [&](uint32_t col) -> uint32_t {
@@ -341,10 +341,8 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
   // forcing ones, 32 span slots, then per warp the row ring, the walk list
   // and results, the ring's mbarriers.
   const uint32_t kc_base = sbase;
-  const uint32_t gc_base = kc_base + cta_cols * 8;
-  const uint32_t kf_base = gc_base + cta_cols * 4;
-  const uint32_t gf_base = kf_base + cta_cols * 8;
-  const uint32_t slots = sbase + (FORCE ? 2 : 1) * cta_cols * 12;
+  const uint32_t kf_base = kc_base + cta_cols * 16;
+  const uint32_t slots = sbase + (FORCE ? 2 : 1) * cta_cols * 16;
   const uint32_t wbase = slots + 128 + warp * G::kWarp;
   const uint32_t ring = wbase;
   const uint32_t stage = ring + G::kSlots * G::kSlot;
@@ -360,7 +358,7 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
   // base row: the CTA's first row.
   const uint32_t ybase =
       static_cast<uint32_t>(a.row0 + a.row_lo + seg_group * a.spc * a.seg_rows);
-  span_put(slots, make_col_keys<FORCE>(kc_base, gc_base, kf_base, gf_base, a.kc_cur, a.kf_cur,
+  span_put(slots, make_col_keys<FORCE>(kc_base, kf_base, a.kc_cur, a.kf_cur,
                                        static_cast<uint32_t>(cta_x0) + 1u, ybase, threadIdx.x,
                                        blockDim.x, cta_cols));
 #if FHPG_PDL
@@ -394,10 +392,8 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
   // words WW-4..WW-1 to padded words 0..3.
   L.padx = (L.w0 + G::kBandWords == L.WW ? 1 : 0) | (L.w0 == 0 ? 2 : 0) | (L.WW << 2);
   Ctx<NW, FORCE> cx;
-  cx.kc = kc_base + bic * G::kBandCols * 8;
-  cx.gc = gc_base + bic * G::kBandCols * 4;
-  cx.kf = kf_base + bic * G::kBandCols * 8;
-  cx.gf = gf_base + bic * G::kBandCols * 4;
+  cx.kc = kc_base + bic * G::kBandCols * 16;
+  cx.kf = kf_base + bic * G::kBandCols * 16;
   cx.ybase = ybase;
   cx.span = min(span_get(slots), a.span_cap);
   cx.x1 = static_cast<uint32_t>(cta_x0 + bic * G::kBandCols) + 1u;
@@ -461,9 +457,9 @@ struct RingGeo {
   static constexpr int kRing = FORCE ? 32 : 56;
 #endif
   static constexpr int kThreads = (kCons + 1) * 32;
-  // Column keys: {lo, t2} and g per column (chirality, then forcing), then
+  // Column keys: {lo, t2, g, 0} per column (chirality, then forcing), then
   // 32 span slots.
-  static constexpr int kKeyTab = G::kBandCols * 12;
+  static constexpr int kKeyTab = G::kBandCols * 16;
   static constexpr int kSpanOff = (FORCE ? 2 : 1) * kKeyTab;
   static constexpr int kKeys = kSpanOff + 128;
   static constexpr int kRingOff = (kKeys + 127) / 128 * 128;
@@ -498,11 +494,11 @@ struct RingGeo {
 // keys' span); returns the new span. Not inlined: it runs a few times per
 // thousand CTA steps.
 template <bool FORCE, int NCONS, int NCOLS>
-__device__ __noinline__ uint32_t rekey_consumers(uint32_t kc, uint32_t gc, uint32_t kf, uint32_t gf,
+__device__ __noinline__ uint32_t rekey_consumers(uint32_t kc, uint32_t kf,
                                                  uint32_t slots, uint64_t kcur, uint64_t kfcur,
                                                  uint32_t x1, uint32_t ybase) {
   asm volatile("bar.sync 2, %0;" ::"n"(NCONS) : "memory");
-  span_put(slots, make_col_keys<FORCE>(kc, gc, kf, gf, kcur, kfcur, x1, ybase, threadIdx.x, NCONS,
+  span_put(slots, make_col_keys<FORCE>(kc, kf, kcur, kfcur, x1, ybase, threadIdx.x, NCONS,
                                        NCOLS));
   if (threadIdx.x == 0) sts32(slots + (NCONS / 32) * 4, 0xFFFFFFFFu);  // the producer's slot
   asm volatile("bar.sync 2, %0;" ::"n"(NCONS) : "memory");
@@ -554,9 +550,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   // (row_lo-1 .. row_lo+nB) from the next whole group on.
   const uint32_t offB = (static_cast<uint32_t>(nA) + 2 + B - 1) / B * B;
   const uint32_t kc_base = sbase;
-  const uint32_t gc_base = kc_base + G::kBandCols * 8;
   const uint32_t kf_base = kc_base + RG::kKeyTab;
-  const uint32_t gf_base = kf_base + G::kBandCols * 8;
   const uint32_t slots = sbase + RG::kSpanOff;
   const uint32_t ring = sbase + RG::kRingOff;
   const uint32_t full = sbase + RG::kBarOff;
@@ -578,7 +572,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   // nothing the previous step wrote, so this overlaps its tail under PDL).
   // Key base row: the part's first destination row.
   auto make_keys = [&](int b, uint32_t ybase, int t0, int nt) {
-    span_put(slots, make_col_keys<FORCE>(kc_base, gc_base, kf_base, gf_base, a.kc_cur, a.kf_cur,
+    span_put(slots, make_col_keys<FORCE>(kc_base, kf_base, a.kc_cur, a.kf_cur,
                                          static_cast<uint32_t>(b * G::kBandCols) + 1u, ybase, t0,
                                          nt, G::kBandCols));
   };
@@ -654,9 +648,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   const uint32_t stage = sbase + RG::kStageOff + warp * G::kStage;
   Ctx<NW, FORCE> cx;
   cx.kc = kc_base;
-  cx.gc = gc_base;
   cx.kf = kf_base;
-  cx.gf = gf_base;
   cx.ybase = static_cast<uint32_t>(a.row0 + RA0);
   cx.span = max(1u, min(span_get(slots), a.span_cap));
   cx.x1 = static_cast<uint32_t>(bA * G::kBandCols) + 1u;
@@ -679,7 +671,7 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
   auto key_end = [&](int Re) { return key_row + static_cast<int>(min(cx.span, static_cast<uint32_t>(Re - key_row))); };
   auto rekey = [&](int b, int row) {
     cx.span = max(1u, min(rekey_consumers<FORCE, RG::kCons * 32, G::kBandCols>(
-                              kc_base, gc_base, kf_base, gf_base, slots, a.kc_cur, a.kf_cur,
+                              kc_base, kf_base, slots, a.kc_cur, a.kf_cur,
                               static_cast<uint32_t>(b * G::kBandCols) + 1u,
                               y0 + static_cast<uint32_t>(row)),
                           a.span_cap));
@@ -855,7 +847,7 @@ void launch_ring(StepArgs a, const CUtensorMap* src, const CUtensorMap* dst, int
 template <int NW, bool FORCE>
 int smem_bytes(int bpc) {
   using G = Geo<NW, FORCE>;
-  return (FORCE ? 2 : 1) * bpc * G::kBandCols * 12 + 128 + kPWarps<NW> * G::kWarp;
+  return (FORCE ? 2 : 1) * bpc * G::kBandCols * 16 + 128 + kPWarps<NW> * G::kWarp;
 }
 
 template <int NW, bool FORCE, int RULE>
