@@ -129,14 +129,20 @@ FHPG_HD uint32_t chir_mask_pre(uint32_t l, uint32_t t2, uint32_t g) {
   const uint32_t lo2 = z1lo ^ ((z1lo >> 27) | (z1hi << 5));
   return static_cast<uint32_t>(static_cast<int32_t>(lo2 * kC2s) >> 31);
 }
-// High word of fin64(K + dy) (the forcing draw, rng.hpp:37-42).
-FHPG_HD uint32_t fin64_hi_pre(uint32_t l, uint32_t t2, uint32_t g) {
+// High word of z2 = (z1 ^ z1 >> 27) * C2, the last product of fin64(K + dy).
+FHPG_HD uint32_t fin64_z2hi_pre(uint32_t l, uint32_t t2, uint32_t g) {
   uint32_t z1lo, z1hi;
   colkey_z1(l, t2, g, z1lo, z1hi);
   const uint32_t ulo = z1lo ^ ((z1lo >> 27) | (z1hi << 5));
   const uint32_t uhi = z1hi ^ (z1hi >> 27);
-  const uint32_t z2hi = static_cast<uint32_t>((static_cast<uint64_t>(ulo) * static_cast<uint32_t>(kC2)) >> 32) +
-                        ulo * static_cast<uint32_t>(kC2 >> 32) + uhi * static_cast<uint32_t>(kC2);
+  return static_cast<uint32_t>((static_cast<uint64_t>(ulo) * static_cast<uint32_t>(kC2)) >> 32) +
+         ulo * static_cast<uint32_t>(kC2 >> 32) + uhi * static_cast<uint32_t>(kC2);
+}
+// High word of fin64(K + dy) (the forcing draw, rng.hpp:37-42). For a
+// bernoulli threshold thr <= 2^31, (hi < thr) == (z2hi < thr): z2hi >= 2^31
+// gives hi >= 2^31 >= thr, else hi = z2hi.
+FHPG_HD uint32_t fin64_hi_pre(uint32_t l, uint32_t t2, uint32_t g) {
+  const uint32_t z2hi = fin64_z2hi_pre(l, t2, g);
   return z2hi ^ (z2hi >> 31);
 }
 

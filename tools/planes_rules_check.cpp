@@ -132,6 +132,12 @@ int main() {
       if (chir_mask_pre(c.lo + dy, c.t2, c.g) != ((f & 1u) ? ~0u : 0u) ||
           fin64_hi_pre(c.lo + dy, c.t2, c.g) != static_cast<uint32_t>(f >> 32))
         ++wrong;
+      // thresholds <= 2^31: z2's high word decides the forcing draw alike
+      // (random thresholds, 2^31 itself, and thresholds next to the value)
+      const uint32_t z2hi = fin64_z2hi_pre(c.lo + dy, c.t2, c.g);
+      const uint64_t near = (z2hi & 0x7FFFFFFFu) + (i & 1);
+      const uint64_t thr = i % 3 == 0 ? (1ull << 31) : i % 3 == 1 ? (mix64(st ^ 11) >> 33) : near;
+      if ((z2hi < thr) != ((f >> 32) < thr)) ++wrong;
     }
     std::printf("col_key_terms: %s (%ld keys)\n", wrong ? "MISMATCH" : "ok", n);
     bad += wrong != 0;
