@@ -64,7 +64,7 @@ constexpr uint32_t kRedSingle = FHPG_LUT((kLC & ~kLA & kLB) | (~kLC & kLA & ~kLB
 // FHP-III, phase 1 output: class masks kept across the chirality walk.
 struct Fhp3Class {
   uint32_t D;      // sites with mass >= 4 (complemented)
-  uint32_t ROT, BB, X, B, AY, KEEP, xp;
+  uint32_t ROT, BB, X, B, AY, xp;  // (keep = none of them: the apply muxes' default)
   uint32_t YE[3];  // Y sites whose axis m is empty (no odd mover)
   uint32_t dep;
 };
@@ -106,8 +106,6 @@ FHPG_HD Fhp3Class fhp3_classify(const uint32_t a[6], uint32_t r, uint32_t s) {
   k.YE[0] = Y & ~O0;
   k.YE[1] = Y & ~O1;
   k.YE[2] = Y & ~O2;
-  const uint32_t t = lop3<kOr3>(k.ROT, k.X, k.B);
-  k.KEEP = lop3<kNor3>(t, k.BB, k.AY);
   // X states (one odd axis o, one pair): the pair's axis is o + 1 (X+) or
   // o - 1 (X-).
   k.xp = lop3<kMux>(O0, P1, lop3<kMux>(O1, P2, P0));
@@ -138,16 +136,21 @@ FHPG_HD void fhp3_apply(const Fhp3Class& k, uint32_t c, uint32_t r, const uint32
   uint32_t PA[3];
 #pragma unroll
   for (int m = 0; m < 3; ++m) PA[m] = lop3<kMux>(c, k.YE[(m + 1) % 3], k.YE[(m + 2) % 3]);
+  // The permutation classes (keep, rotation, bounce-back / pair move) as a
+  // 2-bit source code per site: ROT and e1 = ROT & c | S3 select a_i (keep),
+  // a_{i+1} (rotation, c = 0), a_{i-1} (rotation, c = 1) or a_{i+3} (S3) with
+  // three muxes per direction; U / AY sites override it.
+  const uint32_t e1 = lop3<FHPG_LUT((kLA & kLB) | kLC)>(k.ROT, c, S3);
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
-    const uint32_t rot = lop3<kMux>(c, a[(i + 5) % 6], a[(i + 1) % 6]);
-    uint32_t acc = lop3<kAndOr>(k.ROT, rot, S3 & a[(i + 3) % 6]);
-    acc = lop3<kAndOr>(k.KEEP, a[i], acc);
+    const uint32_t m1 = lop3<kMux>(k.ROT, a[(i + 1) % 6], a[i]);
+    const uint32_t m2 = lop3<kMux>(k.ROT, a[(i + 5) % 6], a[(i + 3) % 6]);
+    const uint32_t m = lop3<kMux>(e1, m2, m1);
     // B -> A, X -> Y: v_{i-1} | v_{i+1}; A -> B (and Y's single): v_{i-1} & v_{i+1}
     const uint32_t q = lop3<FHPG_LUT((kLC & kLA & kLB) | (~kLC & (kLA | kLB)))>(
         v[(i + 5) % 6], v[(i + 1) % 6], k.AY);
-    acc = lop3<kAndOr>(UAY, q, acc);
-    o[i] = lop3<FHPG_LUT((kLA | kLB) ^ kLC)>(acc, PA[i % 3], DN);
+    const uint32_t x = lop3<kMux>(UAY, q, m);
+    o[i] = lop3<FHPG_LUT((kLA | kLB) ^ kLC)>(x, PA[i % 3], DN);
   }
   // The rest flips exactly for B -> A, X -> Y, A -> B, Y -> X (unchanged by D).
   o_r = lop3<FHPG_LUT(kLA ^ (kLB | kLC))>(r, U, k.AY);
