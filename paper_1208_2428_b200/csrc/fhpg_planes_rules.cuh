@@ -136,16 +136,14 @@ FHPG_HD void fhp3_apply(const Fhp3Class& k, uint32_t c, uint32_t r, const uint32
   uint32_t PA[3];
 #pragma unroll
   for (int m = 0; m < 3; ++m) PA[m] = lop3<kMux>(c, k.YE[(m + 1) % 3], k.YE[(m + 2) % 3]);
-  // The permutation classes (keep, rotation, bounce-back / pair move) as a
-  // 2-bit source code per site: ROT and e1 = ROT & c | S3 select a_i (keep),
-  // a_{i+1} (rotation, c = 0), a_{i-1} (rotation, c = 1) or a_{i+3} (S3) with
-  // three muxes per direction; U / AY sites override it.
-  const uint32_t e1 = lop3<FHPG_LUT((kLA & kLB) | kLC)>(k.ROT, c, S3);
+  // The permutation classes as three muxes per direction: keep (a_i) or
+  // bounce-back / pair move (a_{i+3}) by S3, the rotation by the chirality
+  // (c ? a_{i-1} : a_{i+1}), one of the two by ROT; U / AY sites override.
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
-    const uint32_t m1 = lop3<kMux>(k.ROT, a[(i + 1) % 6], a[i]);
-    const uint32_t m2 = lop3<kMux>(k.ROT, a[(i + 5) % 6], a[(i + 3) % 6]);
-    const uint32_t m = lop3<kMux>(e1, m2, m1);
+    const uint32_t m1 = lop3<kMux>(S3, a[(i + 3) % 6], a[i]);
+    const uint32_t rot = lop3<kMux>(c, a[(i + 5) % 6], a[(i + 1) % 6]);
+    const uint32_t m = lop3<kMux>(k.ROT, rot, m1);
     // B -> A, X -> Y: v_{i-1} | v_{i+1}; A -> B (and Y's single): v_{i-1} & v_{i+1}
     const uint32_t q = lop3<FHPG_LUT((kLC & kLA & kLB) | (~kLC & (kLA | kLB)))>(
         v[(i + 5) % 6], v[(i + 1) % 6], k.AY);
@@ -167,9 +165,11 @@ FHPG_HD void fhp3_apply(const Fhp3Class& k, uint32_t c, uint32_t r, const uint32
 //   RC two movers 120 deg apart, no rest (two odd axes, no pair, an even
 //      number of them on odd directions): {i, i+2} -> {i+1}+R        :43-51
 //   obstacles bounce back, rest kept                                   :59-63
-// Only HO depends on the chirality.
+// Only HO depends on the chirality. A symmetric triple has a_{i+3} = ~a_i on
+// every axis, so TB and the obstacles share one selector S3 (out_i =
+// a_{i+3}); keep is the muxes' default.
 struct DefClass {
-  uint32_t HO, TB, RA, RC, KEEP;
+  uint32_t HO, S3, RA, RC, RARC;
   uint32_t dep;
 };
 
@@ -190,36 +190,36 @@ FHPG_HD DefClass def_classify(const uint32_t a[6], uint32_t r, uint32_t s) {
   const uint32_t pi = lop3<kXor3>(a[1], a[3], a[5]);
   constexpr uint32_t kAnB_nC = FHPG_LUT(kLA & kLB & ~kLC);
   k.HO = lop3<kAnB_nC>(noO, oneP, rs);
-  k.TB = lop3<kAnB_nC>(O3, eqv, rs);
+  k.S3 = lop3<kAnB_nC>(O3, eqv, rs) | s;
   k.RA = lop3<FHPG_LUT(kLA & ~kLB & kLC)>(ex1, anyP, r) & ~s;
   k.RC = lop3<FHPG_LUT(kLA & ~kLB & ~kLC)>(ex2, anyP, rs) & ~pi;
-  const uint32_t u = lop3<kOr3>(k.HO, k.TB, k.RA);
-  k.KEEP = lop3<kNor3>(u, k.RC, s);
+  k.RARC = k.RA | k.RC;
   k.dep = k.HO;
   return k;
 }
 
 FHPG_HD void def_apply(const DefClass& k, uint32_t c, uint32_t r, const uint32_t a[6],
                        uint32_t o[6], uint32_t& o_r, uint32_t s) {
+  (void)s;
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     const uint32_t am1 = a[(i + 5) % 6], ap1 = a[(i + 1) % 6];
-    const uint32_t rot = lop3<kMux>(c, am1, a[(i + 4) % 6]);   // c ? a_{i-1} : a_{i-2}
-    const uint32_t t = lop3<FHPG_LUT((kLA & ~kLC) | (kLB & kLC))>(k.TB, k.KEEP, a[i]);
-    const uint32_t acc = lop3<kAndOr>(k.HO, rot, t);
-    const uint32_t ua = lop3<FHPG_LUT((kLA | kLB) & kLC)>(am1, ap1, k.RA);
-    const uint32_t vc = lop3<FHPG_LUT(kLA & kLB & kLC)>(am1, ap1, k.RC);
-    const uint32_t acc2 = lop3<kOr3>(acc, ua, vc);
-    o[i] = lop3<kAndOr>(s, a[(i + 3) % 6], acc2);
+    const uint32_t m1 = lop3<kMux>(k.S3, a[(i + 3) % 6], a[i]);  // bounce / triple, or keep
+    const uint32_t rot = lop3<kMux>(c, am1, a[(i + 4) % 6]);     // c ? a_{i-1} : a_{i-2}
+    const uint32_t m = lop3<kMux>(k.HO, rot, m1);
+    // RA: a_{i-1} | a_{i+1}; RC: a_{i-1} & a_{i+1}
+    const uint32_t q = lop3<FHPG_LUT((kLC & kLA & kLB) | (~kLC & (kLA | kLB)))>(am1, ap1, k.RC);
+    o[i] = lop3<kMux>(k.RARC, q, m);
   }
   o_r = lop3<FHPG_LUT((kLA & ~kLB) | kLC)>(r, k.RA, k.RC);
 }
 
 // FHP-I (fhpg_tables.cpp build_fhp1): head-on pairs without rest rotate by
 // +60 (chirality 1) or -60 degrees (chirality 0), symmetric triples without
-// rest complement, obstacles bounce back; ~30 LOP3 per 32 sites.
+// rest complement, obstacles bounce back (one selector S3, out_i = a_{i+3});
+// ~25 LOP3 per 32 sites.
 struct Fhp1Class {
-  uint32_t HO, TB, KEEP;
+  uint32_t HO, S3;
   uint32_t dep;
 };
 
@@ -235,20 +235,19 @@ FHPG_HD Fhp1Class fhp1_classify(const uint32_t a[6], uint32_t r, uint32_t s) {
   const uint32_t eqv = lop3<FHPG_LUT((kLA & kLB & kLC) | (~kLA & ~kLB & ~kLC))>(a[0], a[2], a[4]);
   constexpr uint32_t kAnB_nC = FHPG_LUT(kLA & kLB & ~kLC);
   k.HO = lop3<kAnB_nC>(noO, oneP, rs);
-  k.TB = lop3<kAnB_nC>(O3, eqv, rs);
-  k.KEEP = lop3<kNor3>(k.HO, k.TB, s);
+  k.S3 = lop3<kAnB_nC>(O3, eqv, rs) | s;
   k.dep = k.HO;
   return k;
 }
 
 FHPG_HD void fhp1_apply(const Fhp1Class& k, uint32_t c, uint32_t r, const uint32_t a[6],
                         uint32_t o[6], uint32_t& o_r, uint32_t s) {
+  (void)s;
 #pragma unroll
   for (int i = 0; i < 6; ++i) {
     const uint32_t rot = lop3<kMux>(c, a[(i + 5) % 6], a[(i + 1) % 6]);  // c ? a_{i-1} : a_{i+1}
-    const uint32_t t = lop3<FHPG_LUT((kLA & ~kLC) | (kLB & kLC))>(k.TB, k.KEEP, a[i]);
-    const uint32_t acc = lop3<kAndOr>(k.HO, rot, t);
-    o[i] = lop3<kAndOr>(s, a[(i + 3) % 6], acc);
+    const uint32_t m1 = lop3<kMux>(k.S3, a[(i + 3) % 6], a[i]);
+    o[i] = lop3<kMux>(k.HO, rot, m1);
   }
   o_r = r;
 }
