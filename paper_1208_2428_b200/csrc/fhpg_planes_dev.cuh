@@ -400,63 +400,42 @@ __device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint3
   return T;
 }
 
-// Walk variant (FHPG_WALK): 0 = the balanced warp walk above; 1 = every lane
-// visits the set bits of its own NW words, one word after the other,
-// highest bit first, and keeps the result bits in registers (no list, no
-// prefix sums, no slice search, no shared-memory results: fewer
-// instructions per row at the price of the warp waiting for its busiest
-// lane).
-#ifndef FHPG_WALK
-#define FHPG_WALK 1
-#endif
+// The step kernels' chirality / forcing walk: every lane visits the set bits
+// of its own NW dep words, one word after the other, highest bit first, and
+// keeps the result bits in registers (no list, no prefix sums, no slice
+// search, no shared-memory results; the balanced walk above costs ~90
+// instructions per lane-row of setup and measured slower). The warp waits
+// for its busiest lane. (Rotating the key table per lane against shared-
+// memory bank conflicts measured 1.6% slower: two more shifts per word.)
 // fn(band column) returns the site's result as a mask (0 or ~0u).
 template <int NW, typename Fn>
 __device__ __forceinline__ void walk_own(const uint32_t (&m)[NW], int lane, uint32_t (&c)[NW],
                                          Fn&& fn) {
+  auto visit = [&](uint32_t mask, uint32_t k0) {
+    uint32_t acc = 0u;
+    while (mask) {
+      const uint32_t j = top_bit(mask);
+      const uint32_t bit = 1u << j;
+      mask ^= bit;
+      acc |= fn(k0 + j) & bit;
+    }
+    return acc;
+  };
   if constexpr (NW == 2) {
-    // The warp waits for its busiest lane in each of the two word loops:
-    // every lane takes its fuller word first, so the first loop's maximum
-    // is over the fuller words and the second's over the emptier ones
-    // (expected 15.0 instead of 16.6 iterations at 12.6% dep sites).
+    // One loop per word: every lane takes its fuller word first, so the
+    // first loop's maximum is over the fuller words and the second's over
+    // the emptier ones (expected 15.0 instead of 16.6 iterations at 12.6%
+    // dep sites).
     const bool sw = __popc(m[1]) > __popc(m[0]);
     const uint32_t kw = static_cast<uint32_t>(lane * 2) * 32u;
-    uint32_t acc0 = 0u, acc1 = 0u;
-    {
-      uint32_t mask = sw ? m[1] : m[0];
-      const uint32_t k0 = kw + (sw ? 32u : 0u);
-      while (mask) {
-        const uint32_t j = top_bit(mask);
-        const uint32_t bit = 1u << j;
-        mask ^= bit;
-        acc0 |= fn(k0 + j) & bit;
-      }
-    }
-    {
-      uint32_t mask = sw ? m[0] : m[1];
-      const uint32_t k1 = kw + (sw ? 0u : 32u);
-      while (mask) {
-        const uint32_t j = top_bit(mask);
-        const uint32_t bit = 1u << j;
-        mask ^= bit;
-        acc1 |= fn(k1 + j) & bit;
-      }
-    }
+    const uint32_t acc0 = visit(sw ? m[1] : m[0], kw + (sw ? 32u : 0u));
+    const uint32_t acc1 = visit(sw ? m[0] : m[1], kw + (sw ? 0u : 32u));
     c[0] = sw ? acc1 : acc0;
     c[1] = sw ? acc0 : acc1;
     return;
   }
 #pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    uint32_t mask = m[w], acc = 0u;
-    const uint32_t kw = static_cast<uint32_t>(lane * NW + w) * 32u;
-    while (mask) {
-      const uint32_t j = top_bit(mask);
-      const uint32_t bit = 1u << j;
-      mask ^= bit;
-      acc |= fn(kw + j) & bit;
-    }
-    c[w] = acc;
-  }
+  for (int w = 0; w < NW; ++w) c[w] = visit(m[w], static_cast<uint32_t>(lane * NW + w) * 32u);
 }
 
 template <int NW, bool FORCE>
@@ -487,12 +466,13 @@ __device__ __forceinline__ uint32_t make_col_keys(uint32_t kc, uint32_t kf, uint
   uint32_t span = 0xFFFFFFFFu;
   for (int c = c0; c < ncols; c += dc) {
     const uint64_t x = static_cast<uint64_t>(x1) + c;
+    const uint32_t pos = static_cast<uint32_t>(c);
     const ColKey k = col_key_terms(column_key(kcur, x) + ybase);
-    sts128(kc + c * 16, k.lo, k.t2, k.g, 0u);
+    sts128(kc + pos * 16, k.lo, k.t2, k.g, 0u);
     span = min(span, colkey_span(k.lo));
     if (FORCE) {
       const ColKey f = col_key_terms(column_key(kfcur, x) + ybase);
-      sts128(kf + c * 16, f.lo, f.t2, f.g, 0u);
+      sts128(kf + pos * 16, f.lo, f.t2, f.g, 0u);
       span = min(span, colkey_span(f.lo));
     }
   }

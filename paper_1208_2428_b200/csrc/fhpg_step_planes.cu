@@ -46,9 +46,6 @@
 
 // 4 words per lane (8 warps per SM) measured slower than 2 (16 warps):
 // 1368 vs 1646 GSUPS on cfg4; build with -DFHPG_PLANES_NW4=4 to select it.
-#ifndef FHPG_STORE_WAIT_LATE
-#define FHPG_STORE_WAIT_LATE 0
-#endif
 #ifndef FHPG_PLANES_NW4
 #define FHPG_PLANES_NW4 2
 #endif
@@ -124,8 +121,8 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, 
     dep[w] = K[w].dep;
   }
   // Chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y)
-  // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76).
-  // (chir_bit: fin64 bit 0 with fewer ALU-pipe instructions.)
+  // = fin64(key[x] + y) (rng.hpp:25-33, step.cpp:73-76), drawn only for the
+  // dep sites, each lane walking its own (walk_own).
   uint32_t o[NW][7];
   // Column keys folded at the band's key base row (fhpg_common.cuh ColKey);
   // rows past their span (a key's low word would cross a 2^30 block) hash
@@ -139,33 +136,14 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, 
   auto chir_slow = [&](uint32_t col) -> uint32_t {
     return chir_mask(column_key(cx.kcur, cx.x1 + col) + y, cx.four);
   };
-#if FHPG_WALK == 0
-  // The previous row's TMA store must have read the staging area (which
-  // also holds the walk scratch) before it is rewritten.
-#if !FHPG_STORE_WAIT_LATE  // timing experiments (1: wait before the outputs, 2: never; wrong results)
-  if (lane == 0) bulk_wait_read();
-  __syncwarp();
-#endif
-  const int T = folded ? walk<NW>(dep, cx.lsm, cx.osm, lane,
-                                  [&](uint32_t col) { return chir_fast(col) & 1u; })
-                       : walk<NW>(dep, cx.lsm, cx.osm, lane,
-                                  [&](uint32_t col) { return chir_slow(col) & 1u; });
-  const uint32_t mine = cx.osm + lane * NW * 4;
-#else
   uint32_t cw[NW];
   if (folded) walk_own<NW>(dep, lane, cw, chir_fast);
   else walk_own<NW>(dep, lane, cw, chir_slow);
-#endif
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
-#if FHPG_WALK == 0
-    const uint32_t c = T ? lds32(mine + w * 4) : 0u;
-#else
-    const uint32_t c = cw[w];
-#endif
     uint32_t oo[6], orr;
     const uint32_t a[6] = {a0[w], a1[w], a2[w], a3[w], a4[w], a5[w]};
-    PlaneRule<RULE>::apply(K[w], c, rr[w], a, oo, orr, so[w]);
+    PlaneRule<RULE>::apply(K[w], cw[w], rr[w], a, oo, orr, so[w]);
 #pragma unroll
     for (int p = 0; p < 6; ++p) o[w][p] = oo[p];
     o[w][6] = orr;
@@ -184,21 +162,6 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, 
       const uint32_t h = static_cast<uint32_t>(fin64(column_key(cx.kfcur, cx.x1 + col) + y) >> 32);
       return static_cast<uint64_t>(h) < cx.thr ? ~0u : 0u;
     };
-#if FHPG_WALK == 0
-    const int TF = folded ? walk<NW>(f, cx.lsm, cx.osm, lane,
-                                     [&](uint32_t col) { return force_fast(col) & 1u; })
-                          : walk<NW>(f, cx.lsm, cx.osm, lane,
-                                     [&](uint32_t col) { return force_slow(col) & 1u; });
-    if (TF) {
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        const uint32_t acc = lds32(mine + w * 4);
-        o[w][5] ^= acc;
-        o[w][2] ^= acc;
-        swaps += __popc(acc);
-      }
-    }
-#else
     uint32_t fw[NW];
     if (!folded) {
       walk_own<NW>(f, lane, fw, force_slow);
@@ -217,14 +180,11 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, 
       o[w][2] ^= fw[w];
       swaps += __popc(fw[w]);
     }
-#endif
   }
-#if FHPG_STORE_WAIT_LATE == 1 || FHPG_WALK != 0
   // The previous row's TMA store must have read the staging area before it
   // is rewritten.
   if (lane == 0) bulk_wait_read();
   __syncwarp();
-#endif
 #pragma unroll
   for (int p = 0; p < 7; ++p) {
     uint32_t v[NW];

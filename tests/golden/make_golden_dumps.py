@@ -63,6 +63,9 @@ def main():
     for c in runs:
         mask = port.cylinder(c["W"], c["H"]) if c.get("geometry") == "cylinder" else None
         state = ref.init(c["W"], c["H"], c["seed"], c["density"], mask)
+        # The obstacle mask of the advancing lattice: every node init_lattice
+        # made solid (the geometry and the wall rows 0 and H-1).
+        mask = (state >> 7).astype(np.uint8)
         swaps = 0
         dumps = []
         for s in range(0, c["steps"], c["every"]):
