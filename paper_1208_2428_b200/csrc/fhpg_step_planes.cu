@@ -412,19 +412,29 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 #ifndef FHPG_RING_CONS
 #define FHPG_RING_CONS 31
 #endif
-template <int NW, bool FORCE>
+// Ring slots (any multiple of the box rows: the consumers track slot indices
+// incrementally). A shallow ring keeps the bands' CTAs on the same rows (a
+// row's 8 band segments leave DRAM together): the memory-bound rules (the
+// reference's DEFAULT, FHP-I: few collisions) run 32 slots (DEFAULT table at
+// cfg4: 2348 GSUPS with 56 slots, 2900 with 32); the compute-bound FHP-III is
+// insensitive (2544 / 2535) and keeps 56; forcing runs 32.
+#ifndef FHPG_RING_SLOTS
+#define FHPG_RING_SLOTS 56
+#endif
+#ifndef FHPG_RING_SLOTS_F
+#define FHPG_RING_SLOTS_F 32
+#endif
+#ifndef FHPG_RING_SLOTS_L
+#define FHPG_RING_SLOTS_L 32
+#endif
+template <int NW, bool FORCE, int RULE = 2>
 struct RingGeo {
   using G = Geo<NW, FORCE>;
   static constexpr int kCons = FHPG_RING_CONS;
-#ifdef FHPG_RING_SLOTS
-  static constexpr int kRing = FORCE ? FHPG_RING_SLOTS_F : FHPG_RING_SLOTS;
-#else
-  // Any multiple of the box rows: the consumers track slot indices
-  // incrementally. 56 is what the folded column keys leave room for
-  // (forcing: 32, 1-3% faster on the forced BASELINE shapes than 56 or 48
-  // before the folded keys).
-  static constexpr int kRing = FORCE ? 32 : 56;
-#endif
+  static constexpr int kRing = FORCE ? FHPG_RING_SLOTS_F
+                               : RULE == 2 ? FHPG_RING_SLOTS : FHPG_RING_SLOTS_L;
+  // (the consumers' slot step wraps once: s + kCons < 2 kRing)
+  static_assert(kRing > kCons, "ring slots > consumer warps");
   static constexpr int kThreads = (kCons + 1) * 32;
   // Column keys: {lo, t2, g, 0} per column (chirality, then forcing), then
   // 32 span slots.
@@ -479,12 +489,12 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar, uint32_t count) {
 }
 
 template <int NW, bool FORCE, int RULE>
-__global__ void __launch_bounds__(RingGeo<NW, FORCE>::kThreads, 1)
+__global__ void __launch_bounds__(RingGeo<NW, FORCE, RULE>::kThreads, 1)
     step_ring_kernel(const __grid_constant__ StepArgs a, const __grid_constant__ CUtensorMap stmap,
                      const __grid_constant__ CUtensorMap sidemap,
                      const __grid_constant__ CUtensorMap map2) {
   using G = Geo<NW, FORCE>;
-  using RG = RingGeo<NW, FORCE>;
+  using RG = RingGeo<NW, FORCE, RULE>;
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5;
@@ -806,7 +816,7 @@ void launch_pdl(K kernel, int grid, int threads, int smem, cudaStream_t st, Args
 template <int NW, bool FORCE, int RULE>
 void launch_ring(StepArgs a, const CUtensorMap* src, const CUtensorMap* dst, int num_sms,
                  cudaStream_t st) {
-  using RG = RingGeo<NW, FORCE>;
+  using RG = RingGeo<NW, FORCE, RULE>;
   const int grid = ring_grid<NW>(a, num_sms);
   ensure_smem_optin(reinterpret_cast<const void*>(step_ring_kernel<NW, FORCE, RULE>), RG::kSmem);
   launch_pdl(step_ring_kernel<NW, FORCE, RULE>, grid, RG::kThreads, RG::kSmem, st, a,
