@@ -51,6 +51,11 @@
 #endif
 
 namespace fhpg {
+#if FHPG_TIMELINE
+constexpr unsigned long long kTimelineMax = 1 << 16;
+__device__ unsigned long long g_timeline[kTimelineMax * 4];
+__device__ unsigned long long g_timeline_n;
+#endif
 namespace {
 
 #include "fhpg_planes_dev.cuh"  // shared device helpers (in this anonymous namespace)
@@ -571,6 +576,10 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE, RULE>::kThreads, 1)
   }
   __syncthreads();
   if (nA + nB <= 0) return;
+#if FHPG_TIMELINE  // timing instrument: CTA start (after the PDL wait) and end, per launch
+  unsigned long long t_start = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
 
   if (warp == RG::kCons) {  // producer (tensor row = local row + 1)
     if (lane == 0) {
@@ -743,6 +752,20 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE, RULE>::kThreads, 1)
     rows_e(bA + 1, row_lo, row_lo + nB, offB, sbase + RG::kCtrOff + 4);
   }
   if (lane == 0) bulk_wait_all();  // the stores have landed before the kernel ends
+#if FHPG_TIMELINE
+  asm volatile("bar.sync 3, %0;" ::"r"(RG::kCons * 32) : "memory");
+  if (threadIdx.x == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    const unsigned long long slot = atomicAdd(&g_timeline_n, 1ull);
+    if (slot < kTimelineMax) {
+      g_timeline[slot * 4 + 0] = blockIdx.x;
+      g_timeline[slot * 4 + 1] = t_start;
+      g_timeline[slot * 4 + 2] = t_end;
+      g_timeline[slot * 4 + 3] = static_cast<unsigned long long>(nA + nB);
+    }
+  }
+#endif
   if (FORCE) {
     unsigned long long sw = swaps;
     for (int o = 16; o; o >>= 1) sw += __shfl_xor_sync(kFull, sw, o);
@@ -1063,4 +1086,19 @@ void launch_unpack_planes(const uint8_t* src, uint8_t* dst, size_t pitch, int W,
   unpack_kernel<<<grid_for(n, num_sms), 256, 0, st>>>(src, dst, pitch, W, nrows);
 }
 
+#if FHPG_TIMELINE
+// Timing instrument (FHPG_TIMELINE builds only; not in include/): copies the
+// recorded (block, start ns, end ns, rows) records out and resets the log.
+extern "C" int fhpg_debug_timeline(unsigned long long* out, int max_records) {
+  unsigned long long n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, g_timeline_n, sizeof(n));
+  if (n > kTimelineMax) n = kTimelineMax;
+  if (static_cast<long long>(n) > max_records) n = max_records;
+  cudaMemcpyFromSymbol(out, g_timeline, n * 4 * sizeof(unsigned long long));
+  const unsigned long long zero = 0;
+  cudaMemcpyToSymbol(g_timeline_n, &zero, sizeof(zero));
+  return static_cast<int>(n);
+}
+#endif
 }  // namespace fhpg

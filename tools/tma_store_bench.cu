@@ -33,7 +33,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 template <int V>
 __global__ void __launch_bounds__(kCons * 32, 1)
     store_k(const __grid_constant__ CUtensorMap m7, const __grid_constant__ CUtensorMap m1,
-            const __grid_constant__ CUtensorMap m72, uint8_t* out, int rows_per_cta) {
+            const __grid_constant__ CUtensorMap m72, uint8_t* out, int rows_per_cta, int drift) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t stage = smem_u32(smem) + warp * 3584;
@@ -41,7 +41,11 @@ __global__ void __launch_bounds__(kCons * 32, 1)
   const int seg = blockIdx.x / kBands;
   const int r0 = seg * rows_per_cta, r1 = min(kRows, r0 + rows_per_cta);
   const int step = V == 4 ? 2 : 1;
-  for (int r = r0 + warp * step; r < r1; r += kCons * step) {
+  // drift: band b starts b * drift rows later in its segment (wrapping), so
+  // the 8 bands of a row are written at different times.
+  const int span = r1 - r0;
+  for (int t = warp * step; t < span; t += kCons * step) {
+    const int r = r0 + (t + band * drift) % span;
     const uint32_t v0 = r * 7 + lane, v1 = r ^ lane;
     if (V == 5) {
       uint8_t* row = out + static_cast<size_t>(r) * kPitch + (32 + band * kBandWords + lane * 2) * 4;
@@ -111,26 +115,26 @@ static CUtensorMap make_map(void* base, unsigned planes, unsigned rows_box) {
 
 template <int V>
 static void run(const CUtensorMap& m7, const CUtensorMap& m1, const CUtensorMap& m72, uint8_t* out,
-                int sms, const char* name) {
+                int sms, const char* name, int drift = 0) {
   const int segs = sms / kBands;
   const int rows_per_cta = (kRows + segs - 1) / segs;
   const int grid = kBands * segs;
   const int smem = kCons * 3584;
   CK(cudaFuncSetAttribute(store_k<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  for (int i = 0; i < 3; ++i) store_k<V><<<grid, kCons * 32, smem>>>(m7, m1, m72, out, rows_per_cta);
+  for (int i = 0; i < 3; ++i) store_k<V><<<grid, kCons * 32, smem>>>(m7, m1, m72, out, rows_per_cta, drift);
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   const int reps = 20;
   CK(cudaEventRecord(a));
-  for (int i = 0; i < reps; ++i) store_k<V><<<grid, kCons * 32, smem>>>(m7, m1, m72, out, rows_per_cta);
+  for (int i = 0; i < reps; ++i) store_k<V><<<grid, kCons * 32, smem>>>(m7, m1, m72, out, rows_per_cta, drift);
   CK(cudaEventRecord(b));
   CK(cudaEventSynchronize(b));
   float ms = 0;
   CK(cudaEventElapsedTime(&ms, a, b));
   const double bytes = static_cast<double>(kRows) * kBands * 1792;
-  printf("%s: %.1f us per step-store, %.0f GB/s, %.0f GSUPS-equivalent store ceiling\n", name,
-         1e3 * ms / reps, bytes / (ms / reps * 1e-3) / 1e9,
+  printf("%s drift %3d: %.1f us per step-store, %.0f GB/s, %.0f GSUPS-equivalent store ceiling\n", name,
+         drift, 1e3 * ms / reps, bytes / (ms / reps * 1e-3) / 1e9,
          static_cast<double>(kRows) * 16384 / (ms / reps * 1e-3) / 1e9);
 }
 
@@ -147,5 +151,6 @@ int main() {
   run<4>(m7, m1, m72, out, sms, "tma3d box{64,7,2}        ");
   run<5>(m7, m1, m72, out, sms, "st.global.v2 direct      ");
   run<6>(m7, m1, m72, out, sms, "tma3d box{64,7,1} no wait");
+  for (int d : {8, 32, 128, 400}) run<0>(m7, m1, m72, out, sms, "tma3d box{64,7,1}        ", d);
   return 0;
 }
