@@ -269,7 +269,11 @@ void sync_layout(fhpg_engine* e) {
 void launch_any(fhpg_engine* e, const fhpg::StepArgs& a) {
   if (e->planes) {
     const int which = a.src == e->base(0) ? 0 : 1;
+#if FHPG_FIXED_SRC  // timing experiment (wrong results): every step reads buffer 0, writes buffer 1
+    e->launches += fhpg::launch_step_planes(a, e->tmap[0], e->tmap[1], e->num_sms,
+#else
     e->launches += fhpg::launch_step_planes(a, e->tmap[which], e->tmap[which ^ 1], e->num_sms,
+#endif
                                             e->stream);
     e->scratch_valid = false;
   } else {
