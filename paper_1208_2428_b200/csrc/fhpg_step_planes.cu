@@ -462,8 +462,15 @@ struct RingGeo {
   static constexpr int kFullBars = kGroups <= 8 ? 32 : kGroups <= 16 ? 64 : 128;
   static_assert(kFullBars > kGroups + (kCons + kBox) / kBox + 1, "tag-free ring bound");
   static_assert(kCons <= 31, "consumer warps");
-  // mbarriers: kFullBars full, kGroups empty.
-  static constexpr int kCtrOff = kBarOff + 8 * (kFullBars + kGroups);
+  // mbarriers: kFullBars full (per group) and the empty barriers: per slot
+  // (3 readers: a consumer releases its three source rows with three plain
+  // arrives, the producer checks the 4 slots of a group; the compute-bound
+  // FHP-III, +1.1%) or per group (12 arrivals, a consumer merges its rows'
+  // arrivals per group; the memory-bound rules, whose producer thread's
+  // per-group cost shows: DEFAULT table 2862 vs 2894).
+  static constexpr bool kSlotEmpty = RULE == 2;
+  static constexpr int kEmpties = kSlotEmpty ? kRing : kGroups;
+  static constexpr int kCtrOff = kBarOff + 8 * (kFullBars + kEmpties);
   // Side buffer of the edge bands: per group, the 4 data words across the
   // periodic wrap of every plane and row ([kBox rows][8 planes][4 words]).
   static constexpr int kSideGroup = kBox * 8 * 16;
@@ -545,11 +552,11 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE, RULE>::kThreads, 1)
   auto edge_of = [&](int b) { return a.nbands == 1 ? 3 : b == 0 ? 1 : b == a.nbands - 1 ? 2 : 0; };
   if (threadIdx.x == 0) {
     // Source rows come in groups of kBox (one TMA box): group P = index /
-    // kBox fills ring group P mod kGroups, completes full barrier P mod
-    // kFullBars and is released on empty barrier P mod kGroups (3 consumers
-    // per row).
+    // kBox fills ring group P mod kGroups and completes full barrier P mod
+    // kFullBars; each slot is released on its own empty barrier (3
+    // consumers per row).
     for (int k = 0; k < RG::kFullBars; ++k) mbar_init(full + k * 8, 1);
-    for (int k = 0; k < RG::kGroups; ++k) mbar_init(empty + k * 8, 3 * RG::kBox);
+    for (int k = 0; k < RG::kEmpties; ++k) mbar_init(empty + k * 8, RG::kSlotEmpty ? 3 : 3 * RG::kBox);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // The band's column keys, made here from the step keys (they depend on
@@ -589,7 +596,14 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE, RULE>::kThreads, 1)
       // k = P mod kG (ring group), lap = P / kG, tracked incrementally
       uint32_t k = 0, lap = 0;
       for (uint32_t P = 0; P < ngroups; ++P) {
-        if (lap > 0) mbar_wait(empty + k * 8, (lap - 1) & 1u);
+        if (lap > 0) {
+          if constexpr (RG::kSlotEmpty) {
+#pragma unroll
+            for (uint32_t q = 0; q < B; ++q) mbar_wait(empty + (B * k + q) * 8, (lap - 1) & 1u);
+          } else {
+            mbar_wait(empty + k * 8, (lap - 1) & 1u);
+          }
+        }
         const uint32_t fb = full + (P % RG::kFullBars) * 8;
         const bool inA = P < gA;
         const int word = (inA ? bA : bA + 1) * G::kBandWords + kPlaneLead - kSlotPad;
@@ -613,8 +627,14 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE, RULE>::kThreads, 1)
         // Ring indices no destination row reads (the tail of part A's last
         // group when part B follows) still count 3 arrivals each, or the
         // slot is never freed.
-        if (nB > 0 && P + 1 == gA && offB > static_cast<uint32_t>(nA) + 2)
-          mbar_arrive(empty + k * 8, 3 * (offB - static_cast<uint32_t>(nA) - 2));
+        if (nB > 0 && P + 1 == gA && offB > static_cast<uint32_t>(nA) + 2) {
+          if constexpr (RG::kSlotEmpty) {
+            for (uint32_t q = static_cast<uint32_t>(nA) + 2; q < offB; ++q)
+              mbar_arrive(empty + (B * k + (q - B * P)) * 8, 3);
+          } else {
+            mbar_arrive(empty + k * 8, 3 * (offB - static_cast<uint32_t>(nA) - 2));
+          }
+        }
         if (++k == kG) {
           k = 0;
           ++lap;
@@ -701,11 +721,11 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE, RULE>::kThreads, 1)
       }
       // Release the three source rows as soon as they are in registers (3
       // consumers per row; segment edges make up for the destination rows
-      // outside [Rb, Re)); one arrive per group the rows fall in (ring group
-      // of slot s = s / B).
+      // outside [Rb, Re)): one arrive per slot, or per group the rows fall
+      // in (ring group of slot s = s / B).
       auto release = [&] {
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0 && !RG::kSlotEmpty) {
           const uint32_t first = first_row ? 1u : 0u, lastr = last_row ? 1u : 0u;
           const uint32_t c0 = 1 + 2 * first, c1 = 1 + first + lastr, c2 = 1 + 2 * lastr;
           const uint32_t g0 = i / B, g1 = (i + 1) / B, g2 = (i + 2) / B;
@@ -714,6 +734,17 @@ __global__ void __launch_bounds__(RingGeo<NW, FORCE, RULE>::kThreads, 1)
           } else {
             mbar_arrive(empty + (sd[0] / B) * 8, c0 + (g1 == g0 ? c1 : 0u));
             mbar_arrive(empty + (sd[2] / B) * 8, c2 + (g1 == g2 ? c1 : 0u));
+          }
+        } else if (lane == 0) {
+          if (!first_row && !last_row) {
+            mbar_arrive(empty + sd[0] * 8, 1);
+            mbar_arrive(empty + sd[1] * 8, 1);
+            mbar_arrive(empty + sd[2] * 8, 1);
+          } else {
+            const uint32_t first = first_row ? 1u : 0u, lastr = last_row ? 1u : 0u;
+            mbar_arrive(empty + sd[0] * 8, 1 + 2 * first);
+            mbar_arrive(empty + sd[1] * 8, 1 + first + lastr);
+            mbar_arrive(empty + sd[2] * 8, 1 + 2 * lastr);
           }
         }
       };
