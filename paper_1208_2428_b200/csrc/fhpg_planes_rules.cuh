@@ -77,32 +77,37 @@ FHPG_HD Fhp3Class fhp3_classify(const uint32_t a[6], uint32_t r, uint32_t s) {
   const uint32_t c3 = lop3<kMaj>(s1, s2, r);
   const uint32_t D = lop3<kMaj>(c1, c2, c3);
   k.D = D;
-  const uint32_t rp = r ^ D;
   // Axis signals: O (odd axis) is unchanged by the reduction; a pair of the
   // reduced state is a pair (D = 0) or an empty axis (D = 1) of the original.
-  const uint32_t O0 = a[0] ^ a[3], O1 = a[1] ^ a[4], O2 = a[2] ^ a[5];
+  // Obstacle sites count every axis as odd (O_k |= s): no fluid class
+  // (ROT, X, B, AY: none or one or two odd axes) then needs its own ~s.
+  constexpr uint32_t kOddOrS = FHPG_LUT((kLA ^ kLB) | kLC);
+  const uint32_t O0 = lop3<kOddOrS>(a[0], a[3], s), O1 = lop3<kOddOrS>(a[1], a[4], s),
+                 O2 = lop3<kOddOrS>(a[2], a[5], s);
   const uint32_t P0 = lop3<kRedAnd>(a[0], a[3], D);
   const uint32_t P1 = lop3<kRedAnd>(a[1], a[4], D);
   const uint32_t P2 = lop3<kRedAnd>(a[2], a[5], D);
   const uint32_t anyP = lop3<kOr3>(P0, P1, P2);
-  k.ROT = lop3<kNor3>(O0, O1, O2) & ~s;
+  k.ROT = lop3<kNor3>(O0, O1, O2);
   const uint32_t ex1 = lop3<FHPG_LUT((kLA ^ kLB ^ kLC) & ~(kLA & kLB & kLC))>(O0, O1, O2);
   const uint32_t ex2 = lop3<FHPG_LUT(((kLA & kLB) | (kLA & kLC) | (kLB & kLC)) & ~(kLA & kLB & kLC))>(O0, O1, O2);
   const uint32_t O3 = lop3<FHPG_LUT(kLA & kLB & kLC)>(O0, O1, O2);
   // Three odd axes (3 movers, no rest): a symmetric triple iff a0 == a2 == a4
   // (invariant under the reduction). Obstacles bounce back too.
   const uint32_t eqv = lop3<FHPG_LUT((kLA & kLB & kLC) | (~kLA & ~kLB & ~kLC))>(a[0], a[2], a[4]);
-  k.BB = lop3<FHPG_LUT(kLA | (kLB & kLC))>(s, O3, eqv);
-  const uint32_t exf1 = ex1 & ~s;
-  k.X = exf1 & anyP;
-  k.B = lop3<FHPG_LUT(kLA & ~kLB & kLC)>(exf1, anyP, rp);
+  k.BB = lop3<FHPG_LUT(kLB & (kLA | kLC))>(s, O3, eqv);  // O3 & (eqv | s)
+  // One odd axis, fluid: with a pair X, without one B (B needs the reduced
+  // rest, r ^ D).
+  k.X = ex1 & anyP;
+  const uint32_t exn = ex1 & ~anyP;
+  k.B = lop3<FHPG_LUT(kLA & (kLB ^ kLC))>(exn, r, D);
   // Two odd axes with movers 120 deg apart <=> both on directions of the
   // same parity <=> an even number of singles on odd directions. With two
   // odd axes the third axis is empty (reduced), i.e. a pair when D = 1, so
   // that parity is a1 ^ a3 ^ a5 ^ D.
-  const uint32_t pi = lop3<kXor3>(a[1], a[3], a[5]) ^ D;
-  k.AY = lop3<FHPG_LUT(kLA & ~kLB & ~kLC)>(ex2, pi, s);
-  const uint32_t Y = k.AY & rp;
+  const uint32_t pi = lop3<kXor3>(a[1], a[3], a[5]);
+  k.AY = lop3<FHPG_LUT(kLA & ~(kLB ^ kLC))>(ex2, pi, D);
+  const uint32_t Y = lop3<FHPG_LUT(kLA & (kLB ^ kLC))>(k.AY, r, D);
   k.YE[0] = Y & ~O0;
   k.YE[1] = Y & ~O1;
   k.YE[2] = Y & ~O2;
