@@ -303,6 +303,25 @@ def test_key_span_cap(W, H, fp, cap, port, tables):
     assert sw == rsw
 
 
+@pytest.mark.parametrize("cap", [1, 7, 0xFFFFFFFF])
+def test_key_span_cap_strips(cap, port, tables):
+    """Re-keying inside the boundary-row launches of a multi-strip engine
+    (interior rows and each strip's first / last row as a second row range
+    of the ring kernel), with forcing; bit-exact with the oracle."""
+    W, H = 4096, 300
+    s, m = port.scramble(W, H, 4242 + (cap & 0xFF))
+    e = P.Engine(W, H, strips=3, devices=[0, 0, 0])
+    e.set_table(tables["fhp3"])
+    e.set_obstacles(m)
+    e.upload(s)
+    e.debug_key_span(cap)
+    sw = e.advance(9, 0.3, 501, 4)
+    ref, rsw = port.advance(s, tables["fhp3"], 9, port.threshold(0.3), 501, 4, mask=m)
+    out = e.download()
+    assert (out == ref).all(), np.argwhere(out != ref)[:5]
+    assert sw == rsw
+
+
 @pytest.mark.parametrize("W,H,fp", [(16384, 1100, 0.0), (16384, 1100, 0.3), (12288, 1500, 0.05),
                                     (16384, 2000, 1.0)])
 def test_ring_extra_ctas(W, H, fp, port, tables):

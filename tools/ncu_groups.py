@@ -1,3 +1,7 @@
+"""Instructions per 32-site word by code region (circuit, hash, walk, ring
+protocol, ...) of one kernel in an ncu capture, with their ALU-pipe share
+and stall samples.
+    python tools/ncu_groups.py <sass.csv> <nvdisasm -g output> <mangled name> <words per launch>"""
 import collections, csv, re, sys
 sass_csv, disasm, fn, words = sys.argv[1], sys.argv[2], sys.argv[3], float(sys.argv[4])
 lines = open(disasm).read().split('\n')
