@@ -480,13 +480,15 @@ __device__ __forceinline__ uint32_t make_col_keys(uint32_t kc, uint32_t kf, uint
 }
 // CTA-wide minimum of the per-thread spans through one slot per warp
 // (slots: 32 words): each warp's lane 0 writes its minimum; after a barrier
-// every thread reads the minimum of all 32 slots.
+// every thread reads the minimum over the CTA's warps' slots.
 __device__ __forceinline__ void span_put(uint32_t slots, uint32_t span) {
   const uint32_t m = __reduce_min_sync(kFull, span);
   if ((threadIdx.x & 31) == 0) sts32(slots + (threadIdx.x >> 5) * 4, m);
 }
 __device__ __forceinline__ uint32_t span_get(uint32_t slots) {
-  return __reduce_min_sync(kFull, lds32(slots + (threadIdx.x & 31) * 4));
+  // (only the slots of the CTA's warps hold values)
+  const uint32_t l = threadIdx.x & 31;
+  return __reduce_min_sync(kFull, l < (blockDim.x >> 5) ? lds32(slots + l * 4) : 0xFFFFFFFFu);
 }
 
 // One destination row. sm, sc, sn: this lane's word address inside plane 0
