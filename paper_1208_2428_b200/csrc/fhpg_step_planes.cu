@@ -432,10 +432,13 @@ __global__ void __launch_bounds__(kPWarps<NW> * 32, 1)
 #ifndef FHPG_RING_SLOTS_L
 #define FHPG_RING_SLOTS_L 32
 #endif
+#ifndef FHPG_RING_CONS_L
+#define FHPG_RING_CONS_L FHPG_RING_CONS  // consumer warps of the memory-bound rules
+#endif
 template <int NW, bool FORCE, int RULE = 2>
 struct RingGeo {
   using G = Geo<NW, FORCE>;
-  static constexpr int kCons = FHPG_RING_CONS;
+  static constexpr int kCons = (FORCE || RULE == 2) ? FHPG_RING_CONS : FHPG_RING_CONS_L;
   static constexpr int kRing = FORCE ? FHPG_RING_SLOTS_F
                                : RULE == 2 ? FHPG_RING_SLOTS : FHPG_RING_SLOTS_L;
   // (the consumers' slot step wraps once: s + kCons < 2 kRing)
