@@ -107,23 +107,24 @@ __device__ __forceinline__ void resident_row(uint32_t sm, uint32_t sc, uint32_t 
   const auto K = PlaneRule<RULE>::classify(a, rr[0], so[0]);
   const uint32_t dep[1] = {K.dep};
   // chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y) (step.cpp:73-76)
-  const int T = walk<1>(dep, lsm, osm, lane,
-                        [&](uint32_t col) { return chir_bit(lds64(kc + col * 8u) + y, four); });
-  const uint32_t c = T ? lds32(osm + lane * 4) : 0u;
+  // (each lane walks its own dep bits, walk_own: no per-row setup — the
+  // rules this kernel runs at small shapes have few dep sites)
+  (void)lsm;
+  (void)osm;
+  uint32_t c[1];
+  walk_own<1>(dep, lane, c, [&](uint32_t col) { return chir_mask(lds64(kc + col * 8u) + y, four); });
   uint32_t o[7];
-  PlaneRule<RULE>::apply(K, c, rr[0], a, o, o[6], so[0]);
+  PlaneRule<RULE>::apply(K, c[0], rr[0], a, o, o[6], so[0]);
   if constexpr (FORCE) {
     // step.cpp:79-88: fluid, W (bit 5) set, E (bit 2) clear after collision
     const uint32_t f[1] = {~so[0] & o[5] & ~o[2]};
-    const int TF = walk<1>(f, lsm, osm, lane, [&](uint32_t col) {
-      return (fin64(lds64(kf + col * 8u) + y) >> 32) < thr ? 1u : 0u;
+    uint32_t acc[1];
+    walk_own<1>(f, lane, acc, [&](uint32_t col) -> uint32_t {
+      return (fin64(lds64(kf + col * 8u) + y) >> 32) < thr ? ~0u : 0u;
     });
-    if (TF) {
-      const uint32_t acc = lds32(osm + lane * 4);
-      o[5] ^= acc;
-      o[2] ^= acc;
-      if (own) swaps += __popc(acc);  // halo rows are counted by their owner CTA
-    }
+    o[5] ^= acc[0];
+    o[2] ^= acc[0];
+    if (own) swaps += __popc(acc[0]);  // halo rows are counted by their owner CTA
   }
 #pragma unroll
   for (int p = 0; p < 7; ++p) sts32(dst + p * P, o[p]);
