@@ -2,7 +2,7 @@
 // (fhpg_step_planes.cu: the streaming ring kernels; fhpg_step_resident.cu:
 // the shared-memory-resident kernel for small lattices): shared-memory and
 // TMA / mbarrier primitives, the rule dispatch, the plane reads of the
-// hexagonal pull and the balanced chirality walk. Included inside an
+// hexagonal pull and the per-lane chirality walk. Included inside an
 // anonymous namespace of namespace fhpg.
 #pragma once
 constexpr unsigned kFull = 0xFFFFFFFFu;
@@ -298,113 +298,12 @@ __device__ __forceinline__ void rd_shr_e(uint32_t a, uint32_t wp, int lane, uint
   o[NW - 1] = __funnelshift_r(v[NW - 1], next, 1);
 }
 
-// Balanced walk over the set bits of the warp's NW * 32 mask words (word
-// i = lane * NW + w <-> band word i, bit j <-> column 32 i + j of the band).
-// The warp's nonzero words go to a list {mask, band column of the word's
-// first bit, sites before it, result word address}; the T sites are
-// split into 32 equal contiguous slices; each lane finds its first word
-// (binary search over the lanes' counts), skips the sites before its slice
-// and visits its sites, advancing through the list (it has no empty words).
-// fn(band column) returns the site's result bit, ORed into the result
-// words (osm). Returns T.
-template <int NW, typename Fn>
-__device__ __forceinline__ int walk(const uint32_t (&m)[NW], uint32_t lsm, uint32_t osm,
-                                    int lane, Fn&& fn) {
-  int cnt = 0, nz = 0;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    cnt += __popc(m[w]);
-    nz += m[w] != 0u;
-  }
-  const int packed = cnt | (nz << 16);
-  int incl = packed;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int v = __shfl_up_sync(kFull, incl, d);
-    if (lane >= d) incl += v;
-  }
-  const int T = __shfl_sync(kFull, incl, 31) & 0xFFFF;
-  if (T == 0) return 0;
-  const int excl = incl - packed;
-  {
-    int q = excl >> 16, c = excl & 0xFFFF;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      if (m[w]) {
-        const uint32_t wi = static_cast<uint32_t>(lane * NW + w);
-        sts128(lsm + q * 16, m[w], wi * 32u, static_cast<uint32_t>(c), osm + wi * 4u);
-        ++q;
-        c += __popc(m[w]);
-      }
-      sts32(osm + (lane * NW + w) * 4, 0u);
-    }
-  }
-  __syncwarp();
-  const int s = (lane * T) >> 5;
-  const int e = ((lane + 1) * T) >> 5;
-  // owner lane of site s: last lane whose exclusive count is <= s
-  const int icnt = incl & 0xFFFF;
-  int o = 0;
-#pragma unroll
-  for (int step = 16; step; step >>= 1) {
-    const int v = __shfl_sync(kFull, icnt, o + step - 1);
-    if (v <= s) o += step;
-  }
-  const int o_excl = __shfl_sync(kFull, excl, o);
-  if (s < e) {
-    uint32_t qa = lsm + (o_excl >> 16) * 16u;  // list entry address
-    uint4 en = lds128(qa);
-#pragma unroll
-    for (int w = 1; w < NW; ++w) {
-      if (s >= static_cast<int>(en.z) + __popc(en.x)) {
-        qa += 16u;
-        en = lds128(qa);
-      }
-    }
-    // Sites are visited lowest bit first (measured a little faster than top
-    // bit first): skip the slice's predecessors.
-    uint32_t mask = en.x, kw = en.y, ow = en.w;
-    for (int k = s - static_cast<int>(en.z); k > 0; --k) mask &= mask - 1u;
-    // site: band column, result word address, bit index
-    // j: bit index, v: 1 << j (the result bit's placement is an IMAD with
-    // v, FMA pipe, where a shift by j would take the ALU pipe)
-    auto next = [&](uint32_t& ka, uint32_t& wa, uint32_t& v) {
-      if (mask == 0u) {
-        qa += 16u;
-        const uint4 n = lds128(qa);
-        mask = n.x;
-        kw = n.y;
-        ow = n.w;
-      }
-      v = mask & (0u - mask);
-      mask ^= v;
-      ka = kw + top_bit(v);
-      wa = ow;
-    };
-    int it = s;
-    for (; it + 1 < e; it += 2) {
-      uint32_t k0, w0, v0, k1, w1, v1;
-      next(k0, w0, v0);
-      next(k1, w1, v1);
-      const uint32_t b0 = fn(k0), b1 = fn(k1);
-      red_or(w0, b0 * v0);
-      red_or(w1, b1 * v1);
-    }
-    if (it < e) {
-      uint32_t k0, w0, v0;
-      next(k0, w0, v0);
-      red_or(w0, fn(k0) * v0);
-    }
-  }
-  __syncwarp();
-  return T;
-}
-
 // The step kernels' chirality / forcing walk: every lane visits the set bits
 // of its own NW dep words, one word after the other, highest bit first, and
 // keeps the result bits in registers (no list, no prefix sums, no slice
-// search, no shared-memory results; the balanced walk above costs ~90
-// instructions per lane-row of setup and measured slower). The warp waits
+// search, no shared-memory results; a balanced warp walk — a list of the
+// nonzero words, prefix sums, equal slices per lane — costs ~90
+// instructions per lane-row of setup and measured slower, see git history). The warp waits
 // for its busiest lane. (Rotating the key table per lane against shared-
 // memory bank conflicts measured 1.6% slower: two more shifts per word.)
 // fn(band column) returns the site's result as a mask (0 or ~0u).

@@ -8,32 +8,22 @@
 // collide_rows with its counter-RNG chirality and forcing (step.cpp:63-93),
 // bit-exactly.
 //
-// Layout. A lattice row holds 8 bit planes (0-5 movers NW..W, 6 rest, 7
-// obstacle); bit j of word i of a plane = column 32 i + j. Each plane row is
-// W/32 words plus 4 pad words on either side holding the periodic wrap
-// (words W/32-4 .. W/32-1 on the left, 0 .. 3 on the right), so a row is
-// W + 256 bytes and every band's row, edges included, is one rectangular
-// TMA box. Pitch, halo rows and spare rows follow the byte layout. The
-// obstacle plane is static: the pack kernel writes it into both ping-pong
-// buffers and the step never does, so a step moves the algorithmic 15 bits
-// per site (8 planes read, 7 written) plus the pad words.
+// Layout (fhpg_kernels.cuh). A lattice row holds 8 bit planes (0-5 movers
+// NW..W, 6 rest, 7 obstacle); bit j of word i of a plane = column 32 i + j.
+// A plane row is 32 lead words, the W/32 data words and 32 trail words (the
+// data starts on a 128-byte line). The obstacle plane is static: the pack
+// kernel writes it into both ping-pong buffers and the step never does, so a
+// step moves the algorithmic 15 bits per site (8 planes read, 7 written).
 //
-// Work decomposition. A warp owns a band of 32 * NW words (1024 NW columns)
-// and a segment of rows that it streams top to bottom; lane l holds words
-// [l NW, l NW + NW) of every plane. Each source row is loaded once (one
-// NW-word vector load per plane and lane, two rows in flight) and turned on
-// arrival into the shifted planes the three destination rows need: the
-// +-1 column moves of the hexagonal pull are funnel shifts with the
-// neighbour lane's edge word (SHFL) or, at band edges, the neighbour band's
-// word (one scalar load per shifted plane, periodic wrap).
-//
-// Collision: bit-sliced circuit on 32 sites per instruction. Chirality is
-// drawn only where the outcome depends on it: the dep masks of the warp's
-// row go to shared memory, the warp splits the dep sites evenly over its
-// lanes (prefix sum), each lane evaluates fin64_bit0(column key + row) for
-// its slice (keys staged in shared memory) and sets the chirality bits with
-// shared-memory ORs. Forcing (thr > 0) is resolved the same way on the
-// post-collision candidates (fluid, W set, E clear).
+// Kernels. step_ring_kernel (W % 2048 == 0): one CTA per SM = a band of 2048
+// columns x a segment of rows; a producer warp streams the segment's source
+// rows into a shared ring with 4-row TMA boxes, 31 consumer warps take
+// destination rows round-robin (lane l: words 2l, 2l+1 of every plane),
+// evaluate the circuit, draw the chirality / forcing bits of the sites that
+// need them (walk_own over folded column keys) and store the 7 output planes
+// with one TMA store per row. step_planes_kernel (W = 1024 x odd): per-warp
+// rings, the same row code. See DESIGN.md for the measured design choices.
+
 #include <cstdint>
 #include <type_traits>
 
