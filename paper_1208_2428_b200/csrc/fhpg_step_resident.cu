@@ -54,6 +54,18 @@ struct ResArgs {
   unsigned* bar;           // grid barrier: [0] arrivals, [1] generation
 };
 
+// u / n for the small run-time divisors of the index loops (bands, 16-byte
+// chunks per row / plane) without the ~20-instruction integer division:
+// with m = ceil(2^32 / n), umulhi(u, m) is exact for u < 2^32 / n.
+struct FastDiv {
+  uint32_t n, m;
+  __device__ explicit FastDiv(uint32_t d)
+      : n(d), m(d > 1 ? static_cast<uint32_t>(((1ull << 32) + d - 1) / d) : 0u) {}
+  __device__ __forceinline__ uint32_t div(uint32_t u) const { return n == 1 ? u : __umulhi(u, m); }
+};
+// x mod n for x in [-n, 2n).
+__device__ __forceinline__ int wrap_mod(int x, int n) { return x < 0 ? x + n : x >= n ? x - n : x; }
+
 __device__ __forceinline__ uint4 ldcg128(const void* p) {
   return __ldcg(reinterpret_cast<const uint4*>(p));  // L2 only: other SMs wrote it
 }
@@ -146,6 +158,8 @@ __global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a
   const uint32_t GP = static_cast<uint32_t>(plane_stride_words(a.W)) * 4u;  // global plane row
   const uint32_t RB = 8u * P;                              // row of 8 planes
   const int nb = a.W >> 10;                                // 1024-column bands
+  const FastDiv dnb(nb), dn16(RB / 16u), dp16(P / 16u);
+  const FastDiv dsn16(7u * ((WW + 2 * kPlaneWrap) / 4u)), dsp16((WW + 2 * kPlaneWrap) / 4u);
   const int k = a.depth;
   const int r0 = blockIdx.x * a.rows_per_cta, r1 = min(a.H, r0 + a.rows_per_cta);
   const int base = r0 - k - 1;  // global row of local row 0
@@ -171,9 +185,9 @@ __global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a
       const uint32_t n16 = RB / 16u, p16 = P / 16u;
       const uint32_t total = static_cast<uint32_t>(hi - lo) * n16;
       for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
-        const uint32_t rr = t / n16, c = t % n16, pl = c / p16, j = c % p16;
+        const uint32_t rr = dn16.div(t), c = t - rr * n16, pl = dp16.div(c), j = c - pl * p16;
         const int d = static_cast<int>(4 * j) - 4;  // data word of the chunk
-        const uint32_t gw = kPlaneLead + static_cast<uint32_t>((d + WW) % WW);
+        const uint32_t gw = kPlaneLead + static_cast<uint32_t>(wrap_mod(d, WW));
         const uint4 v = ldcg128((g ? a.g1 : a.g0) + static_cast<size_t>(lo + rr) * a.pitch +
                                 pl * GP + gw * 4u);
         sts128(bufs + static_cast<uint32_t>(lo + rr - base) * RB + c * 16u, v.x, v.y, v.z, v.w);
@@ -193,7 +207,8 @@ __global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a
       const uint32_t dst = bufs + static_cast<uint32_t>(sb ^ 1) * bufsz;
       const int units = (chi - clo) * nb;
       for (int u = warp; u < units; u += kResWarps) {
-        const int r = clo + u / nb, b = u % nb;
+        const int q = static_cast<int>(dnb.div(static_cast<uint32_t>(u)));
+        const int r = clo + q, b = u - q * nb;
         const uint32_t off = static_cast<uint32_t>(r - base) * RB + static_cast<uint32_t>(4 + b * 32 + lane) * 4u;
         const int pad = (b == 0 && lane < 4) ? WW * 4 : (b == nb - 1 && lane >= 28) ? -WW * 4 : 0;
         const uint32_t y = static_cast<uint32_t>(r);
@@ -218,9 +233,9 @@ __global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a
       const uint32_t total = static_cast<uint32_t>(r1 - r0) * n16;
       const uint32_t src = bufs + static_cast<uint32_t>(sb) * bufsz;
       for (uint32_t t = threadIdx.x; t < total; t += blockDim.x) {
-        const uint32_t rr = t / n16, c = t % n16, pl = c / p16, j = c % p16;
+        const uint32_t rr = dsn16.div(t), c = t - rr * n16, pl = dsp16.div(c), j = c - pl * p16;
         const int d = static_cast<int>(4 * j) - kPlaneWrap;  // data word of the chunk
-        const uint32_t sw = 4u + static_cast<uint32_t>((d + WW) % WW);
+        const uint32_t sw = 4u + static_cast<uint32_t>(wrap_mod(d, WW));
         const uint4 v = lds128(src + static_cast<uint32_t>(r0 + rr - base) * RB + pl * P + sw * 4u);
         __stcg(reinterpret_cast<uint4*>((g ? a.g0 : a.g1) + static_cast<size_t>(r0 + rr) * a.pitch +
                                         pl * GP + (kPlaneLead - kPlaneWrap + 4 * j) * 4u),

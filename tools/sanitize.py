@@ -19,6 +19,8 @@ cases = [  # W, H, force_p, rule, path, key span cap, strips
     (2048, 64, 0.2, "fhp3", "streaming", None, None),
     (4096, 131, 0.0, "fhp3", "streaming", None, None),
     (4096, 70, 0.3, "default", "streaming", None, None),
+    (4096, 70, 0.0, "fhp1", "streaming", None, None),
+    (16384, 1100, 0.0, "default", "streaming", 50, None),
     (4096, 70, 0.3, "fhp3", "streaming", 3, None),
     (16384, 1100, 0.0, "fhp3", "streaming", None, None),
     (16384, 1100, 0.01, "fhp3", "streaming", 100, None),
