@@ -151,3 +151,23 @@ def test_local_strips_gpu_equal_single_engine(n, port, tables):
         wc = whole.cells(4)
         for k in range(4):
             assert (sum(c[k] for c in cells) == wc[k]).all()
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_bench_spawns_its_own_ranks(n):
+    """`python bench.py --gpus N` outside torchrun re-executes itself under
+    torch.distributed.run with N ranks (the driver's SCALE invocation); each
+    rank takes its row strip of the weak-scaled N x 16384-row lattice."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n),
+                        "--dry-run"], capture_output=True, text=True, timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(s) for s in r.stdout.splitlines() if s.startswith("{")]
+    assert sorted(d["rank"] for d in lines) == list(range(n))
+    assert all(d["world"] == n and d["H"] == 16384 * n for d in lines)
+    rows = sorted(tuple(d["rows"]) for d in lines)
+    assert rows == strip_rows(16384 * n, n)
