@@ -35,9 +35,21 @@ namespace {
 
 #include "fhpg_planes_dev.cuh"
 
-constexpr int kResWarps = 16;
-constexpr int kResThreads = kResWarps * 32;
-constexpr int kResScratch = 16 * 32 + 4 * 32;  // walk list (32 entries) + result words (32)
+// Warps per CTA and halo depth per kind of run (tools/ab_small.py, cfg1 =
+// FHP-I 1024^2 p = 0; FHP-III p = 0.01 at 1024^2 / 2048^2): a k-step block
+// computes rows_per_cta + 2 (k - 1 - j) rows at its step j, so with 7 rows
+// per CTA 24 warps take every step of a depth-9 block in one row round
+// (16 warps: 3 of 8 steps in two): cfg1 539 -> 569 GSUPS. The forced runs
+// (two walks per row, twice the key table) keep 16 warps and depth 8
+// (1024^2: 313 vs 306 with 24 warps).
+#ifndef FHPG_RES_WARPS
+#define FHPG_RES_WARPS 24
+#endif
+#ifndef FHPG_RES_WARPS_F
+#define FHPG_RES_WARPS_F 16
+#endif
+template <bool FORCE>
+constexpr int res_warps() { return FORCE ? FHPG_RES_WARPS_F : FHPG_RES_WARPS; }
 
 struct ResArgs {
   uint8_t* g0;             // the engine's two plane buffers, local row 0
@@ -101,8 +113,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
 // offset of this word's periodic-wrap copy (0: none).
 template <int RULE, bool FORCE, int Q>
 __device__ __forceinline__ void resident_row(uint32_t sm, uint32_t sc, uint32_t sn, uint32_t dst,
-                                             uint32_t P, int pad, uint32_t kc, uint32_t kf,
-                                             uint32_t lsm, uint32_t osm, int lane, uint32_t y,
+                                             uint32_t P, int pad, uint32_t kc, uint32_t kf, int lane, uint32_t y,
                                              uint32_t four, uint64_t thr, bool own, unsigned& swaps) {
   uint32_t a0[1], a1[1], a2[1], a3[1], a4[1], a5[1], rr[1], so[1];
   // Pull sources (backends.cpp:64-73): k0 (x+q, r+1), k1 (x+q-1, r+1),
@@ -121,8 +132,6 @@ __device__ __forceinline__ void resident_row(uint32_t sm, uint32_t sc, uint32_t 
   // chirality: bit 0 of node_random(seed, Chirality, step, x + 1, y) (step.cpp:73-76)
   // (each lane walks its own dep bits, walk_own: no per-row setup — the
   // rules this kernel runs at small shapes have few dep sites)
-  (void)lsm;
-  (void)osm;
   uint32_t c[1];
   walk_own<1>(dep, lane, c, [&](uint32_t col) { return chir_mask(lds64(kc + col * 8u) + y, four); });
   uint32_t o[7];
@@ -149,7 +158,8 @@ __device__ __forceinline__ void resident_row(uint32_t sm, uint32_t sc, uint32_t 
 }
 
 template <int RULE, bool FORCE>
-__global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a) {
+__global__ void __launch_bounds__(res_warps<FORCE>() * 32, 1) step_resident_kernel(ResArgs a) {
+  constexpr int kResWarps = res_warps<FORCE>();
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -167,8 +177,6 @@ __global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a
   const uint32_t kc = sbase, kf = sbase + a.W * 8;
   const uint32_t bufs = sbase + (FORCE ? 2u : 1u) * static_cast<uint32_t>(a.W) * 8u;
   const uint32_t bufsz = static_cast<uint32_t>(nloc) * RB;
-  const uint32_t lsm = bufs + 2u * bufsz + static_cast<uint32_t>(warp) * kResScratch;
-  const uint32_t osm = lsm + 16 * 32;
   // Zero rows stand for the rows outside the lattice.
   for (uint32_t o = threadIdx.x * 16u; o < 2u * bufsz; o += blockDim.x * 16u) sts128(bufs + o, 0, 0, 0, 0);
   unsigned swaps = 0;
@@ -215,11 +223,11 @@ __global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a
         const bool own = r >= r0 && r < r1;
         if (r & 1)
           resident_row<RULE, FORCE, 1>(src + off - RB, src + off, src + off + RB, dst + off, P, pad,
-                                       kc + b * 8192, kf + b * 8192, lsm, osm, lane, y, a.k4, a.thr,
+                                       kc + b * 8192, kf + b * 8192, lane, y, a.k4, a.thr,
                                        own, swaps);
         else
           resident_row<RULE, FORCE, 0>(src + off - RB, src + off, src + off + RB, dst + off, P, pad,
-                                       kc + b * 8192, kf + b * 8192, lsm, osm, lane, y, a.k4, a.thr,
+                                       kc + b * 8192, kf + b * 8192, lane, y, a.k4, a.thr,
                                        own, swaps);
       }
       __syncthreads();
@@ -253,29 +261,42 @@ __global__ void __launch_bounds__(kResThreads, 1) step_resident_kernel(ResArgs a
   }
 }
 
-int resident_smem(int W, int H, int rows_per_cta, int depth, bool force) {
+int resident_smem(int W, int rows_per_cta, int depth, bool force) {
   const int RB = 8 * (W / 32 + 8) * 4;
   const int nloc = rows_per_cta + 2 * depth + 2;
-  (void)H;
-  return (force ? 2 : 1) * W * 8 + 2 * nloc * RB + kResWarps * kResScratch;
+  return (force ? 2 : 1) * W * 8 + 2 * nloc * RB;
 }
 
 }  // namespace
 
+// Halo depth (steps per block), unforced / forced. Unforced: cfg1 with 16
+// warps 2 -> 320, 4 -> 416, 8 -> 422, 12 -> 397 GSUPS (round 2 start); with
+// 24 warps depth 9 fills every row round (569 vs 564 at depth 8).
 #ifndef FHPG_RESIDENT_DEPTH
-#define FHPG_RESIDENT_DEPTH 8  // cfg1 (1024^2 FHP-I): 2 -> 320, 4 -> 416, 8 -> 422, 12 -> 397 GSUPS
+#define FHPG_RESIDENT_DEPTH 9
+#endif
+#ifndef FHPG_RESIDENT_DEPTH_F
+#define FHPG_RESIDENT_DEPTH_F 8
 #endif
 // Largest lattice (sites) the resident kernel takes: above it the streaming
-// kernels' per-launch cost is a small fraction of a step.
+// kernels' per-launch cost is a small fraction of a step. Measured crossover
+// (tools/ab_small.py AB_WIDE=1, GSUPS resident / streaming): unforced 2048^2
+// FHP-I 1205 / 1045, FHP-III 866 / 860; forced FHP-III 2048 x 1024 395 / 376,
+// 2048^2 597 / 671 — the forced runs switch at 2M sites.
 #ifndef FHPG_RESIDENT_MAX_SITES
 #define FHPG_RESIDENT_MAX_SITES (4LL << 20)
 #endif
+#ifndef FHPG_RESIDENT_MAX_SITES_F
+#define FHPG_RESIDENT_MAX_SITES_F (2LL << 20)
+#endif
 
 int resident_plan(int W, int H, uint64_t thr, int num_sms, int* rows_per_cta, int* grid) {
-  if (W % 1024 || H < 3 || static_cast<long long>(W) * H > FHPG_RESIDENT_MAX_SITES) return 0;
+  const bool force = thr != 0;
+  const long long max_sites = force ? FHPG_RESIDENT_MAX_SITES_F : FHPG_RESIDENT_MAX_SITES;
+  if (W % 1024 || H < 3 || static_cast<long long>(W) * H > max_sites) return 0;
   const int rpc = (H + num_sms - 1) / num_sms;
-  const int depth = FHPG_RESIDENT_DEPTH;
-  if (resident_smem(W, H, rpc, depth, thr != 0) > 227 * 1024) return 0;
+  const int depth = force ? FHPG_RESIDENT_DEPTH_F : FHPG_RESIDENT_DEPTH;
+  if (resident_smem(W, rpc, depth, force) > 227 * 1024) return 0;
   *rows_per_cta = rpc;
   *grid = (H + rpc - 1) / rpc;
   return depth;
@@ -304,14 +325,15 @@ int launch_step_resident(uint8_t* const g[2], int cur, size_t pitch, int W, int 
   a.k4 = 4u;
   a.swaps = swaps;
   a.bar = bar;
-  const int smem = resident_smem(W, H, rpc, depth, thr != 0);
+  const bool f = thr != 0;
+  const int smem = resident_smem(W, rpc, depth, f);
   void* args[] = {&a};
   auto go = [&](auto kernel) {
     ensure_smem_optin(reinterpret_cast<const void*>(kernel), smem);
     *err = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3(grid),
-                                       dim3(kResThreads), args, smem, st);
+                                       dim3((f ? res_warps<true>() : res_warps<false>()) * 32),
+                                       args, smem, st);
   };
-  const bool f = thr != 0;
   if (rule == 0) f ? go(step_resident_kernel<0, true>) : go(step_resident_kernel<0, false>);
   else if (rule == 1) f ? go(step_resident_kernel<1, true>) : go(step_resident_kernel<1, false>);
   else f ? go(step_resident_kernel<2, true>) : go(step_resident_kernel<2, false>);

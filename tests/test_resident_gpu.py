@@ -74,3 +74,15 @@ def test_mixed_single_and_multi_step_calls(W, H, port, tables):
         b = _engine(W, H, t, mask, state, "streaming")
         b.advance(2, 0.0, 40, step - 40)
         assert (a.download() == b.download()).all()
+
+
+def test_resident_plan_crossover():
+    """The resident kernel takes unforced lattices up to 4M sites and forced
+    ones up to 2M (measured crossovers, fhpg_step_resident.cu): 2048^2 runs
+    resident unforced and streaming forced; 2048 x 1024 resident either way."""
+    big = P.Engine(2048, 2048)
+    assert big.resident_depth(0.0) > 0 and big.resident_depth(0.01) == 0
+    half = P.Engine(2048, 1024)
+    assert half.resident_depth(0.0) > 0 and half.resident_depth(0.01) > 0
+    big.close()
+    half.close()

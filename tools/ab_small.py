@@ -1,11 +1,15 @@
 """Interleaved A/B of lib/ab/<v>.so variants on the small (resident-kernel)
 shapes: cfg1 (FHP-I 1024^2, rest particles cleared, 1000 steps) and two
-forced FHP-III shapes. Device-timed (tools/bench_configs.timed).
+forced FHP-III shapes (AB_WIDE=1: three more around the resident / streaming
+crossover). Device-timed (tools/bench_configs.timed).
     python tools/ab_small.py v1 v2 ..."""
 import json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASES = [(1024, 1024, "fhp1", 0.0, 1000, True), (1024, 1024, "fhp3", 0.01, 1000, False),
          (2048, 2048, "fhp3", 0.01, 500, False)]
+if os.environ.get("AB_WIDE"):  # the resident / streaming crossover shapes
+    CASES += [(2048, 1024, "fhp3", 0.01, 1000, False), (2048, 2048, "fhp1", 0.0, 500, True),
+              (2048, 2048, "fhp3", 0.0, 500, False)]
 for rnd in (1, 2):
     for v in sys.argv[1:]:
         out = []
