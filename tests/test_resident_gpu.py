@@ -76,13 +76,15 @@ def test_mixed_single_and_multi_step_calls(W, H, port, tables):
         assert (a.download() == b.download()).all()
 
 
-def test_resident_plan_crossover():
+def test_resident_plan_crossover(tables):
     """The resident kernel takes unforced lattices up to 4M sites and forced
     ones up to 2M (measured crossovers, fhpg_step_resident.cu): 2048^2 runs
     resident unforced and streaming forced; 2048 x 1024 resident either way."""
     big = P.Engine(2048, 2048)
+    big.set_table(tables["fhp3"])  # a circuit rule: the bit-plane layout
     assert big.resident_depth(0.0) > 0 and big.resident_depth(0.01) == 0
     half = P.Engine(2048, 1024)
+    half.set_table(tables["fhp3"])
     assert half.resident_depth(0.0) > 0 and half.resident_depth(0.01) > 0
     big.close()
     half.close()
