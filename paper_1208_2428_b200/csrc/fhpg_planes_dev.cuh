@@ -306,17 +306,17 @@ __device__ __forceinline__ void rd_shr_e(uint32_t a, uint32_t wp, int lane, uint
 // instructions per lane-row of setup and measured slower, see git history). The warp waits
 // for its busiest lane. (Rotating the key table per lane against shared-
 // memory bank conflicts measured 1.6% slower: two more shifts per word.)
-// fn(band column) returns the site's result as a mask (0 or ~0u).
-template <int NW, typename Fn>
-__device__ __forceinline__ void walk_own(const uint32_t (&m)[NW], int lane, uint32_t (&c)[NW],
-                                         Fn&& fn) {
+// step(acc, bit, band column) folds one visited site's result bit into acc.
+template <int NW, typename Step>
+__device__ __forceinline__ void walk_core(const uint32_t (&m)[NW], int lane, uint32_t (&c)[NW],
+                                          Step&& step) {
   auto visit = [&](uint32_t mask, uint32_t k0) {
     uint32_t acc = 0u;
     while (mask) {
       const uint32_t j = top_bit(mask);
       const uint32_t bit = 1u << j;
       mask ^= bit;
-      acc |= fn(k0 + j) & bit;
+      acc = step(acc, bit, k0 + j);
     }
     return acc;
   };
@@ -335,6 +335,32 @@ __device__ __forceinline__ void walk_own(const uint32_t (&m)[NW], int lane, uint
   }
 #pragma unroll
   for (int w = 0; w < NW; ++w) c[w] = visit(m[w], static_cast<uint32_t>(lane * NW + w) * 32u);
+}
+// fn(band column) returns the site's result as a mask (0 or ~0u).
+template <int NW, typename Fn>
+__device__ __forceinline__ void walk_own(const uint32_t (&m)[NW], int lane, uint32_t (&c)[NW],
+                                         Fn&& fn) {
+  walk_core<NW>(m, lane, c,
+                [&](uint32_t acc, uint32_t bit, uint32_t col) { return acc | (fn(col) & bit); });
+}
+#ifndef FHPG_WALK_PRED
+#define FHPG_WALK_PRED 1
+#endif
+// The same walk for a result "h(column) < thr" (the forcing draw): the
+// compare's predicate guards the OR directly (ISETP + @P LOP3 instead of
+// ISETP + SEL + LOP3: one ALU-pipe instruction less per visited site).
+template <int NW, typename Fn>
+__device__ __forceinline__ void walk_own_lt(const uint32_t (&m)[NW], int lane, uint32_t (&c)[NW],
+                                            uint32_t thr, Fn&& h) {
+  walk_core<NW>(m, lane, c, [&](uint32_t acc, uint32_t bit, uint32_t col) {
+#if FHPG_WALK_PRED
+    asm("{\n\t.reg .pred q;\n\tsetp.lt.u32 q, %1, %2;\n\t@q or.b32 %0, %0, %3;\n\t}"
+        : "+r"(acc) : "r"(h(col)), "r"(thr), "r"(bit));
+    return acc;
+#else
+    return acc | (h(col) < thr ? bit : 0u);
+#endif
+  });
 }
 
 template <int NW, bool FORCE>

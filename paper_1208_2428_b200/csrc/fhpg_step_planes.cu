@@ -162,9 +162,9 @@ __device__ __forceinline__ void dest_row(uint32_t sm, uint32_t sc, uint32_t sn, 
       walk_own<NW>(f, lane, fw, force_slow);
     } else if (cx.thr <= (1ull << 31)) {  // p <= 1/2: compare z2's high word
       const uint32_t thr = static_cast<uint32_t>(cx.thr);
-      walk_own<NW>(f, lane, fw, [&](uint32_t col) -> uint32_t {
+      walk_own_lt<NW>(f, lane, fw, thr, [&](uint32_t col) -> uint32_t {
         const uint4 k = lds128(cx.kf + col * 16u);
-        return fin64_z2hi_pre(k.x + dy, k.y, k.z) < thr ? ~0u : 0u;
+        return fin64_z2hi_pre(k.x + dy, k.y, k.z);
       });
     } else {
       walk_own<NW>(f, lane, fw, force_fast);
