@@ -240,6 +240,19 @@ int grid_for(long long n, int threads, int num_sms) {
   return static_cast<int>(g < 1 ? 1 : g);
 }
 
+// SM count of the current device (grid-stride helpers size their grids by
+// it), cached per device.
+int current_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+  if (dev >= 0 && dev < 64) cache[dev] = n;
+  return n;
+}
+
 }  // namespace
 
 bool fast_path_ok(int W) { return W >= 32 && W % 16 == 0 && W % 512 != 16; }
@@ -279,20 +292,20 @@ void launch_column_keys(uint64_t* zc, uint64_t* zf, uint64_t kc, uint64_t kf, in
 
 void launch_apply_mask(uint8_t* base, const uint8_t* mask, size_t pitch, int W, int nrows,
                        cudaStream_t st) {
-  apply_mask_kernel<<<grid_for(static_cast<long long>(nrows) * W, 256, 148), 256, 0, st>>>(
+  apply_mask_kernel<<<grid_for(static_cast<long long>(nrows) * W, 256, current_sms()), 256, 0, st>>>(
       base, mask, pitch, W, nrows);
 }
 
 void launch_init(uint8_t* base, const uint8_t* mask, size_t pitch, int W, int nrows,
                  long long row0, long long H, uint64_t seed, uint64_t thr, cudaStream_t st) {
   const uint64_t kinit = step_key(seed, kInit, 0);
-  init_kernel<<<grid_for(static_cast<long long>(nrows) * W, 256, 148), 256, 0, st>>>(
+  init_kernel<<<grid_for(static_cast<long long>(nrows) * W, 256, current_sms()), 256, 0, st>>>(
       base, mask, pitch, W, nrows, row0, H, seed, thr, kinit);
 }
 
 void launch_reduce_global(const uint8_t* base, size_t pitch, int W, int nrows, long long* acc,
                           cudaStream_t st) {
-  reduce_global_kernel<<<grid_for(static_cast<long long>(nrows) * W, 256, 148), 256, 0, st>>>(
+  reduce_global_kernel<<<grid_for(static_cast<long long>(nrows) * W, 256, current_sms()), 256, 0, st>>>(
       base, pitch, W, nrows, acc);
 }
 
@@ -300,7 +313,7 @@ void launch_reduce_cells(const uint8_t* base, size_t pitch, int W, int nrows, lo
                          long long H, int B, int* nodes, int* particles, long long* px,
                          long long* py, cudaStream_t st) {
   const int cells_x = (W + B - 1) / B;
-  reduce_cells_kernel<<<grid_for(static_cast<long long>(nrows) * cells_x, 256, 148), 256, 0,
+  reduce_cells_kernel<<<grid_for(static_cast<long long>(nrows) * cells_x, 256, current_sms()), 256, 0,
                         st>>>(base, pitch, W, nrows, row0, H, B, cells_x, nodes, particles, px,
                               py);
 }
