@@ -306,18 +306,43 @@ __device__ __forceinline__ void rd_shr_e(uint32_t a, uint32_t wp, int lane, uint
 // instructions per lane-row of setup and measured slower, see git history). The warp waits
 // for its busiest lane. (Rotating the key table per lane against shared-
 // memory bank conflicts measured 1.6% slower: two more shifts per word.)
+#ifndef FHPG_LOP3P
+#define FHPG_LOP3P 1
+#endif
+// a ^ b and whether it is nonzero, from one LOP3 with a predicate output
+// (PTX lop3.or.b32 d|p): the walk's mask update doubles as its loop test
+// (no separate ISETP per visited site).
+__device__ __forceinline__ uint32_t xor_nonzero(uint32_t a, uint32_t b, bool& nonzero) {
+  uint32_t d, nz;
+  asm("{\n\t.reg .pred p;\n\tlop3.or.b32 %0|p, %2, %3, 0, 0x3c, 0;\n\tselp.u32 %1, 1, 0, p;\n\t}"
+      : "=r"(d), "=r"(nz) : "r"(a), "r"(b));
+  nonzero = nz != 0u;
+  return d;
+}
 // step(acc, bit, band column) folds one visited site's result bit into acc.
 template <int NW, typename Step>
 __device__ __forceinline__ void walk_core(const uint32_t (&m)[NW], int lane, uint32_t (&c)[NW],
                                           Step&& step) {
   auto visit = [&](uint32_t mask, uint32_t k0) {
     uint32_t acc = 0u;
+#if FHPG_LOP3P
+    if (mask) {
+      bool more;
+      do {
+        const uint32_t j = top_bit(mask);
+        const uint32_t bit = 1u << j;
+        mask = xor_nonzero(mask, bit, more);
+        acc = step(acc, bit, k0 + j);
+      } while (more);
+    }
+#else
     while (mask) {
       const uint32_t j = top_bit(mask);
       const uint32_t bit = 1u << j;
       mask ^= bit;
       acc = step(acc, bit, k0 + j);
     }
+#endif
     return acc;
   };
   if constexpr (NW == 2) {
